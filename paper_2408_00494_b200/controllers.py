@@ -1,0 +1,467 @@
+"""Drop-in controller API backed by the sm_100a kernels.
+
+Mirrors the reference module ``belief_mppi.controllers`` (read-only at
+/root/reference/pkg/src/belief_mppi/controllers.py): same class and function
+names, constructor and ``control_step`` signatures, validation errors and
+exceptions.  Instances of the reference's own dataclasses are accepted
+(duck-typed) wherever ours are.
+
+Numerics: all rollouts, belief moments, costs and the weighted update run
+in ``libbssmppi.so`` (csrc/).  Two noise sources:
+
+* ``noise_source="philox"`` (default, performance mode): control and belief
+  normals come from the in-kernel Philox4x32-10 generator keyed by the
+  reference's (seed, *run_path, domain, iteration) identity;
+* ``noise_source="reference"`` (oracle-noise mode): the normals are drawn
+  from the reference's own numpy substreams (controllers.py:384-393,
+  285-287) and shipped to the device, so results track the reference
+  step for step within FP32 tolerance.
+
+There is no CPU fallback: without a CUDA device every compute call raises.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib, streams
+from .belief import DEFAULT_SUBSET
+from .constraints import SafetyParams, allocate_budget, backoff_gaussian
+from .dynamics import CONTROL_DIM, DEFAULT_NOISE_CHANNELS, IDX_VX, NoiseModel, phys_vector, psd_factor
+
+CONTROLLER_KINDS = ("mppi", "smppi", "bss")
+NOISE_SOURCES = ("philox", "reference")
+
+
+class AllRolloutsInvalid(RuntimeError):
+    """Every sampled trajectory left the frame / produced a non-finite cost."""
+
+
+@dataclass(frozen=True)
+class ControlBounds:
+    delta_max: float = 0.35
+    throttle_min: float = -1.0
+    throttle_max: float = 1.0
+
+    def __post_init__(self):
+        if self.delta_max <= 0.0 or self.throttle_max <= self.throttle_min:
+            raise ValueError("invalid control bounds")
+
+    @property
+    def lower(self):
+        return np.array([-self.delta_max, self.throttle_min])
+
+    @property
+    def upper(self):
+        return np.array([self.delta_max, self.throttle_max])
+
+    def clamp(self, u):
+        return np.clip(u, self.lower, self.upper)
+
+
+@dataclass(eq=False)
+class MppiConfig:
+    """Sampling configuration (reference controllers.py:71-105).  Note the
+    reference's naming: ``samples`` = K control sequences, ``horizon`` = T,
+    ``inner_samples`` = M Monte-Carlo realisations per sequence."""
+
+    kind: str = "bss"
+    samples: int = 256
+    horizon: int = 20
+    temperature: float = 1.0
+    control_cost_weight: float = 0.1
+    sigma_eps: np.ndarray = None
+    bounds: ControlBounds = field(default_factory=ControlBounds)
+    inner_samples: int = 16
+    persist_particles: bool = False
+
+    def __post_init__(self):
+        if self.kind not in CONTROLLER_KINDS:
+            raise ValueError(f"unknown controller kind {self.kind!r}")
+        if self.samples < 1 or self.horizon < 1:
+            raise ValueError("samples and horizon must be >= 1")
+        if self.temperature <= 0.0:
+            raise ValueError("temperature must be > 0")
+        if self.kind == "bss" and self.inner_samples < 2:
+            raise ValueError("bss controller needs inner_samples >= 2")
+        if self.sigma_eps is None:
+            self.sigma_eps = np.diag([0.15 ** 2, 0.35 ** 2])
+        sig = np.atleast_2d(np.asarray(self.sigma_eps, dtype=float))
+        if sig.shape == (1, CONTROL_DIM):
+            sig = np.diag(sig[0])
+        if sig.shape != (CONTROL_DIM, CONTROL_DIM):
+            raise ValueError("sigma_eps must be a 2x2 covariance or a diagonal pair")
+        psd_factor(sig)
+        self.sigma_eps = sig
+        self.precision = np.linalg.pinv(sig)
+
+
+@dataclass(eq=False)
+class CostSpec:
+    """Running cost (reference controllers.py:108-138)."""
+
+    q_diag: np.ndarray = None
+    v_goal: float = 6.0
+    obstacle_penalty: float = 10000.0
+    terminal_scale: float = 1.0
+    safety: SafetyParams = field(default_factory=SafetyParams)
+    backoff: float = None
+    belief_stage_cost: callable = None
+
+    def __post_init__(self):
+        if self.q_diag is None:
+            self.q_diag = np.array([6.0, 0.0, 0.02, 0.0, 0.0, 0.2, 0.1, 0.0])
+        if self.backoff is None:
+            self.backoff = backoff_gaussian(allocate_budget(0.05, 2)[0])
+        self.q_diag = np.asarray(self.q_diag, dtype=float)
+        if self.q_diag.shape != (8,) or np.any(self.q_diag < 0.0):
+            raise ValueError("q_diag must be 8 nonnegative weights")
+        if self.obstacle_penalty < 0.0:
+            raise ValueError("obstacle_penalty must be >= 0")
+
+    def goal_state(self):
+        g = np.zeros(8)
+        g[IDX_VX] = self.v_goal
+        return g
+
+
+@dataclass
+class ControlPlan:
+    controls: np.ndarray
+
+    def __post_init__(self):
+        self.controls = np.asarray(self.controls, dtype=float)
+        if self.controls.ndim != 2 or self.controls.shape[1] != CONTROL_DIM:
+            raise ValueError("plan must have shape (K, 2)")
+
+    @classmethod
+    def zeros(cls, horizon: int):
+        return cls(np.zeros((horizon, CONTROL_DIM)))
+
+    def shifted(self):
+        """Warm start: drop the executed entry, repeat the final one."""
+        return ControlPlan(np.concatenate([self.controls[1:], self.controls[-1:]]))
+
+
+@dataclass
+class RolloutBatch:
+    controls: np.ndarray
+    perturbations: np.ndarray
+    costs: np.ndarray = None
+
+
+@dataclass(eq=False)
+class RolloutContext:
+    model: object
+    track: object
+    cost: CostSpec
+    noise: NoiseModel = None
+    subset: object = field(default_factory=lambda: DEFAULT_SUBSET)
+
+    def __post_init__(self):
+        if self.noise is None:
+            self.noise = NoiseModel(np.zeros((3, 3)))
+
+
+# ---------------------------------------------------------------- problem packing
+
+def _bounds_arrays(bounds):
+    return (np.array([-bounds.delta_max, bounds.throttle_min], dtype=float),
+            np.array([bounds.delta_max, bounds.throttle_max], dtype=float))
+
+
+def _check_supported(ctx, cost):
+    sub = tuple(getattr(ctx.subset, "indices", ctx.subset))
+    if sub != tuple(DEFAULT_SUBSET.indices):
+        raise NotImplementedError(f"device path tracks the default subset {DEFAULT_SUBSET.indices}, got {sub}")
+    if tuple(ctx.noise.channels) != tuple(DEFAULT_NOISE_CHANNELS):
+        raise NotImplementedError("device path adds process noise on (vx, vy, yaw rate) only")
+    if getattr(ctx.model, "integrator", "euler") != "euler":
+        raise NotImplementedError("controller model must use the Euler integrator")
+    if getattr(cost, "belief_stage_cost", None) is not None:
+        raise NotImplementedError("belief_stage_cost hooks are arbitrary Python; not evaluable in-kernel")
+
+
+def build_problem(kind, K, T, M, temperature, gamma, sigma_eps, precision, bounds, persist,
+                  ctx, k_begin=0, k_count=None):
+    """Pack reference-typed objects into the C ``bssmppi_problem``.
+    Returns (problem, keepalive) -- the track arrays must outlive create()."""
+    cost = ctx.cost
+    _check_supported(ctx, cost)
+    p = _lib.Problem()
+    p.kind = _lib.KIND[kind]
+    p.samples = int(K)
+    p.horizon = int(T)
+    p.inner_samples = int(M)
+    p.persist_particles = int(bool(persist))
+    p.temperature = float(temperature)
+    p.control_cost_weight = float(gamma)
+    sig = np.asarray(sigma_eps, dtype=float)
+    p.sigma_factor[:] = psd_factor(sig).reshape(-1).tolist()
+    prec = np.zeros((2, 2)) if precision is None else np.asarray(precision, dtype=float)
+    p.precision[:] = prec.reshape(-1).tolist()
+    lo, hi = _bounds_arrays(bounds)
+    p.bounds_lo[:] = lo.tolist()
+    p.bounds_hi[:] = hi.tolist()
+    p.q_diag[:] = np.asarray(cost.q_diag, dtype=float).tolist()
+    p.v_goal = float(cost.v_goal)
+    p.obstacle_penalty = float(cost.obstacle_penalty)
+    p.terminal_scale = float(cost.terminal_scale)
+    p.cbf_rate = float(cost.safety.cbf_rate)
+    p.penalty = float(cost.safety.penalty)
+    p.backoff = float(cost.backoff)
+    p.phys[:] = phys_vector(ctx.model).tolist()
+    p.dt = float(ctx.model.dt)
+    p.noise_factor[:] = np.asarray(ctx.noise.factor, dtype=float).reshape(-1).tolist()
+    s = np.ascontiguousarray(ctx.track.s, dtype=np.float64)
+    kap = np.ascontiguousarray(ctx.track.kappa, dtype=np.float64)
+    p.track_s = _lib.dptr(s)
+    p.track_kappa = _lib.dptr(kap)
+    p.track_n = s.size
+    p.track_length = float(ctx.track.length)
+    p.half_width = float(ctx.track.half_width)
+    p.track_closed = int(bool(ctx.track.closed))
+    p.k_begin = int(k_begin)
+    p.k_count = int(K - k_begin if k_count is None else k_count)
+    return p, (s, kap)
+
+
+class DeviceContext:
+    """Owns one ``bssmppi_ctx`` (device buffers for one K-shard)."""
+
+    def __init__(self, problem, device=0, stream=None):
+        lib = _lib.load()
+        h = _lib.C.c_void_p()
+        _lib.check(lib.bssmppi_create(_lib.C.byref(problem), int(device), _lib.C.byref(h)))
+        self.h = h
+        self.lib = lib
+        self.T = problem.horizon
+        self.k_count = problem.k_count
+        if stream is not None:
+            _lib.check(lib.bssmppi_set_stream(h, _lib.C.c_void_p(int(stream))))
+
+    def close(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            self.lib.bssmppi_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _status(code):
+    if code == _lib.ERR_ALL_INVALID:
+        raise AllRolloutsInvalid("no rollout produced a finite cost")
+    if code == _lib.ERR_INVALID:
+        raise ValueError(_lib.load().bssmppi_last_error().decode())
+    _lib.check(code)
+
+
+# ---------------------------------------------------------------- functional surface
+
+def sample_controls(plan: ControlPlan, sigma_eps, n_samples: int, rng, bounds) -> RolloutBatch:
+    """Reference controllers.py:166-177: eps = z F^T, u = clip(v + eps).
+    The normals come from the caller's numpy generator exactly as in the
+    reference; the factor product and clamp run on the device."""
+    v = np.ascontiguousarray(plan.controls, dtype=np.float64)
+    T = v.shape[0]
+    factor = np.ascontiguousarray(psd_factor(np.atleast_2d(np.asarray(sigma_eps, dtype=float))))
+    z = np.ascontiguousarray(rng.standard_normal((n_samples, T, CONTROL_DIM)))
+    eps = np.empty_like(z)
+    u = np.empty_like(z)
+    lo, hi = _bounds_arrays(bounds)
+    lib = _lib.load()
+    _status(lib.bssmppi_sample_controls(n_samples, T, _lib.dptr(z), _lib.dptr(factor.reshape(-1).copy()),
+                                        _lib.dptr(v), _lib.dptr(lo), _lib.dptr(hi), _lib.dptr(eps),
+                                        _lib.dptr(u)))
+    return RolloutBatch(controls=u, perturbations=eps)
+
+
+def mppi_update(batch: RolloutBatch, temperature: float, bounds) -> ControlPlan:
+    """Reference controllers.py:180-194, FP64 on the device."""
+    costs = np.ascontiguousarray(batch.costs, dtype=np.float64)
+    u = np.ascontiguousarray(batch.controls, dtype=np.float64)
+    K, T, _ = u.shape
+    lo, hi = _bounds_arrays(bounds)
+    out = np.empty((T, CONTROL_DIM))
+    diag = _lib.Diag()
+    _status(_lib.load().bssmppi_mppi_update(K, T, _lib.dptr(costs), _lib.dptr(u), float(temperature),
+                                            _lib.dptr(lo), _lib.dptr(hi), _lib.dptr(out),
+                                            _lib.C.byref(diag)))
+    return ControlPlan(out)
+
+
+def mppi_weights(costs, temperature: float):
+    """Reference controllers.py:180-187 (diagnostic helper, host numpy:
+    never on the control path, which folds the weights into the device
+    update)."""
+    costs = np.asarray(costs, dtype=float)
+    finite = np.isfinite(costs)
+    if not finite.any():
+        raise AllRolloutsInvalid("no rollout produced a finite cost")
+    return np.exp(-(costs - costs[finite].min()) / temperature)
+
+
+class DeviceKey(tuple):
+    """Pass as ``rng`` to request device Philox normals keyed by (k0, k1)."""
+
+
+def _rollout(kind, x0, cov0, batch, nominal, ctx, precision, cost_weight, rng=None,
+             inner_samples=0, persist_particles=False, moments=False, device=0):
+    u = np.ascontiguousarray(batch.controls, dtype=np.float64)
+    eps = np.ascontiguousarray(batch.perturbations, dtype=np.float64)
+    K, T, _ = u.shape
+    if kind == "bss" and (rng is None or inner_samples < 2):
+        raise ValueError("bss rollouts need an rng and inner_samples >= 2")
+    M = int(inner_samples) if kind == "bss" else 1
+    prob, keep = build_problem(kind, K, T, M, 1.0, cost_weight, np.eye(2), precision,
+                               ControlBounds(), persist_particles, ctx)
+    dc = DeviceContext(prob, device)
+    z = key = None
+    if kind == "bss":
+        if isinstance(rng, DeviceKey):
+            key = _lib.key_arr(rng)
+        else:   # the reference's single draw per rollout (controllers.py:285-287)
+            z = np.ascontiguousarray(rng.standard_normal((T, K, M, 7)), dtype=np.float32)
+    costs = np.empty(K)
+    mom = np.empty((T, K, 18), dtype=np.float32) if (moments and kind == "bss") else None
+    x0 = np.ascontiguousarray(x0, dtype=np.float64)
+    cov0 = None if cov0 is None else np.ascontiguousarray(cov0, dtype=np.float64)
+    nom = np.ascontiguousarray(nominal, dtype=np.float64)
+    try:
+        _status(dc.lib.bssmppi_rollout(dc.h, _lib.dptr(x0), _lib.dptr(cov0), _lib.dptr(u),
+                                       _lib.dptr(eps), _lib.dptr(nom), _lib.fptr(z), key,
+                                       _lib.dptr(costs), _lib.fptr(mom)))
+    finally:
+        dc.close()
+        del keep
+    return (costs, mom) if moments else costs
+
+
+def rollout_mppi(x0, batch, nominal, ctx, precision=None, cost_weight: float = 0.0):
+    return _rollout("mppi", x0, None, batch, nominal, ctx, precision, cost_weight)
+
+
+def rollout_smppi(x0, batch, nominal, ctx, precision=None, cost_weight: float = 0.0):
+    return _rollout("smppi", x0, None, batch, nominal, ctx, precision, cost_weight)
+
+
+def rollout_bss(mean0, cov0, batch, nominal, ctx, rng, inner_samples: int, precision=None,
+                cost_weight: float = 0.0, persist_particles: bool = False, moments: bool = False):
+    """Belief-space rollout costs (reference controllers.py:252-258).  With a
+    numpy ``rng`` the reference's own normals are consumed; with a
+    ``DeviceKey`` the in-kernel Philox generator is used.  ``moments=True``
+    additionally returns the per-step raw belief moments (T, K, 18)."""
+    return _rollout("bss", mean0, cov0, batch, nominal, ctx, precision, cost_weight, rng,
+                    inner_samples, persist_particles, moments)
+
+
+# ---------------------------------------------------------------- controller
+
+class Controller:
+    """Receding-horizon sampling controller (reference controllers.py:343-410).
+
+    Extra keyword-only options (defaults keep the reference call shape):
+    ``noise_source`` ("philox" | "reference"), ``device`` (CUDA ordinal),
+    ``stream`` (cudaStream_t as int).  After each ``control_step`` the
+    attribute ``last_diagnostics`` holds v+, the cost minimum/argmin, the
+    number of finite rollouts, the effective sample size and the device
+    time of the iteration.
+    """
+
+    def __init__(self, config, cost, model, track, noise=None, subset=None, seed: int = 0,
+                 run_path=(), *, noise_source: str = "philox", device: int = 0, stream=None):
+        if noise_source not in NOISE_SOURCES:
+            raise ValueError(f"noise_source must be one of {NOISE_SOURCES}")
+        self.config = config
+        self.ctx = RolloutContext(model=model, track=track, cost=cost, noise=noise,
+                                  subset=subset if subset is not None else DEFAULT_SUBSET)
+        _check_supported(self.ctx, cost)
+        self.seed = int(seed)
+        self.run_path = tuple(int(p) for p in run_path)
+        self.plan = ControlPlan.zeros(config.horizon)
+        self.iteration = 0
+        self.noise_source = noise_source
+        self.device = int(device)
+        self.stream = stream
+        self.last_diagnostics = None
+        self._dev = None   # created lazily: no CUDA before a fork (sim.py:321-322)
+
+    # -- internals
+    def _stream(self, domain):
+        return streams.substream(self.seed, *self.run_path, domain, self.iteration)
+
+    def _key(self, domain):
+        return _lib.key_arr(streams.device_key(self.seed, *self.run_path, domain, self.iteration))
+
+    def _k_range(self):
+        return 0, self.config.samples
+
+    def _device_ctx(self):
+        if self._dev is None:
+            cfg = self.config
+            k0, kn = self._k_range()
+            M = cfg.inner_samples if cfg.kind == "bss" else 1
+            prob, keep = build_problem(cfg.kind, cfg.samples, cfg.horizon, M, cfg.temperature,
+                                       cfg.control_cost_weight, cfg.sigma_eps, cfg.precision,
+                                       cfg.bounds, cfg.persist_particles, self.ctx, k0, kn)
+            self._dev = DeviceContext(prob, self.device, self.stream)
+            del keep
+        return self._dev
+
+    def _noise_arrays(self):
+        """Oracle-noise mode: the reference's exact draws for this iteration."""
+        cfg = self.config
+        k0, kn = self._k_range()
+        factor = psd_factor(np.atleast_2d(np.asarray(cfg.sigma_eps, dtype=float)))
+        zc = self._stream(streams.DOMAIN_CONTROL).standard_normal((cfg.samples, cfg.horizon, 2))
+        eps = np.ascontiguousarray((zc @ factor.T)[k0:k0 + kn])
+        z = None
+        if cfg.kind == "bss":
+            zb = self._stream(streams.DOMAIN_BELIEF).standard_normal(
+                (cfg.horizon, cfg.samples, cfg.inner_samples, 7))
+            z = np.ascontiguousarray(zb[:, k0:k0 + kn], dtype=np.float32)
+        return eps, z
+
+    def _inputs(self, state, cov):
+        x0 = np.ascontiguousarray(state, dtype=np.float64).reshape(8)
+        cov0 = None if cov is None else np.ascontiguousarray(cov, dtype=np.float64).reshape(16)
+        plan = np.ascontiguousarray(self.plan.controls, dtype=np.float64)
+        if plan.shape != (self.config.horizon, CONTROL_DIM):
+            raise ValueError("plan shape does not match the horizon")
+        if self.noise_source == "reference":
+            eps, z = self._noise_arrays()
+            kc = kb = None
+        else:
+            eps = z = None
+            kc, kb = self._key(streams.DOMAIN_CONTROL), self._key(streams.DOMAIN_BELIEF)
+        return x0, cov0, plan, kc, kb, eps, z
+
+    def _finish(self, vplus, diag):
+        self.last_diagnostics = dict(vplus=vplus.copy(), **diag.as_dict())
+        optimized = ControlPlan(vplus)
+        self.plan = optimized.shifted()
+        self.iteration += 1
+        return optimized.controls[0].copy(), self.plan
+
+    def control_step(self, state, cov=None):
+        """One receding-horizon iteration (reference controllers.py:374-410).
+        Returns (applied control (2,), next plan) and advances the warm start."""
+        dev = self._device_ctx()
+        x0, cov0, plan, kc, kb, eps, z = self._inputs(state, cov)
+        vplus = np.empty((self.config.horizon, CONTROL_DIM))
+        diag = _lib.Diag()
+        _status(dev.lib.bssmppi_control_step(dev.h, _lib.dptr(x0), _lib.dptr(cov0), _lib.dptr(plan), kc,
+                                             kb, _lib.dptr(eps), _lib.fptr(z), _lib.dptr(vplus),
+                                             _lib.C.byref(diag)))
+        return self._finish(vplus, diag)
+
+    def close(self):
+        if self._dev is not None:
+            self._dev.close()
+            self._dev = None

@@ -1,0 +1,78 @@
+// Counter-based normal generator for performance mode.
+//
+// Philox4x32-10 (Salmon et al., SC'11) keyed per (seed, run_path, domain,
+// iteration) -- the same identity as the reference's keyed numpy substreams
+// (streams.py:21-28) -- with counters built from (t, global k, m), so every
+// normal is a pure function of its coordinates: results do not depend on
+// grid shape, K-sharding or launch order.
+#pragma once
+#include <cstdint>
+
+namespace bss {
+
+struct Philox4 {
+  uint32_t x, y, z, w;
+};
+
+__host__ __device__ __forceinline__ uint32_t mulhi32(uint32_t a, uint32_t b) {
+#ifdef __CUDA_ARCH__
+  return __umulhi(a, b);
+#else
+  return (uint32_t)(((uint64_t)a * (uint64_t)b) >> 32);
+#endif
+}
+
+__host__ __device__ __forceinline__ Philox4 philox4x32_10(Philox4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int i = 0; i < 10; ++i) {
+    const uint32_t hi0 = mulhi32(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    const uint32_t hi1 = mulhi32(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = Philox4{hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0};
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return c;
+}
+
+#ifdef __CUDACC__
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Box-Muller pair from two 32-bit words.  Uniforms are built by bit
+// insertion (no I2F on the XU pipe): u1 in (0, 1], angle in [-pi, pi).
+__device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float &z0, float &z1) {
+  const float u1 = 2.0f - __uint_as_float(0x3f800000u | (a >> 9));
+  const float u2 = __uint_as_float(0x3f800000u | (b >> 9)) - 1.5f;
+  const float r = sqrt_approx(-1.38629436112f * __log2f(u1));  // sqrt(-2 ln u1)
+  float s, c;
+  __sincosf(6.28318530718f * u2, &s, &c);
+  z0 = r * c;
+  z1 = r * s;
+}
+
+// The 7 standard normals of particle-step (t, k, m): [0:4] re-projection
+// on the tracked subset, [4:7] process noise -- the column layout of the
+// reference's z_all block (controllers.py:285-287, belief.py:328-333).
+__device__ __forceinline__ void belief_normals(uint32_t k0, uint32_t k1, uint32_t t, uint32_t kg,
+                                               uint32_t m, float z[7]) {
+  const Philox4 a = philox4x32_10(Philox4{t, m, kg, 0u}, k0, k1);
+  const Philox4 b = philox4x32_10(Philox4{t, m, kg, 1u}, k0, k1);
+  float spare;
+  box_muller(a.x, a.y, z[0], z[1]);
+  box_muller(a.z, a.w, z[2], z[3]);
+  box_muller(b.x, b.y, z[4], z[5]);
+  box_muller(b.z, b.w, z[6], spare);
+}
+
+// The 2 standard normals of control sample (k, t) (controllers.py:175).
+__device__ __forceinline__ void control_normals(uint32_t k0, uint32_t k1, uint32_t t, uint32_t kg,
+                                                float &z0, float &z1) {
+  const Philox4 a = philox4x32_10(Philox4{t, kg, 0x5eedc0deu, 0u}, k0, k1);
+  box_muller(a.x, a.y, z0, z1);
+}
+#endif
+
+}  // namespace bss

@@ -1,0 +1,415 @@
+// Fused BSS-MPPI rollout kernel (sampling -> belief rollouts -> cost).
+//
+// Restates the reference hot loop (controllers.py:261-341 `_rollout`,
+// belief.py:311-335 `propagate_mc_batch`, belief.py:227-308 Cholesky /
+// sample build / moments, constraints.py:130-186 DCBF + shield penalty,
+// controllers.py:166-177 + 215-228 sampling and costs) as ONE kernel:
+//
+//   * one group of G lanes (G = min(32, pow2 >= M)) owns one rollout k and
+//     its M Monte-Carlo particles (lane l handles m = l, l+G, ...); with
+//     M >= 32 a warp is one rollout and no block-level sync exists at all;
+//   * particles never touch memory: re-projection x = mu + L z, the Euler
+//     step, process noise and the moment sums all stay in registers;
+//   * per-step moments use a shift c = step(mu_t) (the noise-free particle),
+//     accumulating S1 = sum(x - c), S2 = sum((x - c)(x - c)^T) in ONE pass,
+//     reduced across the group with a reduce-scatter shuffle butterfly and
+//     all-gathered through 20 floats of shared memory; mean = c + S1/M,
+//     cov = (S2 - S1 S1^T / M)/(M-1).  Algebraically the reference's
+//     two-pass estimator; deviations from the shift are O(sigma) so FP32
+//     keeps tree-sum accuracy, and a zero-spread cloud collapses onto the
+//     deterministic step exactly (belief.py:282-284 guarantee);
+//   * everything per (k, t) -- control sample, clamp, control cost, stage
+//     cost, Cholesky, DCBF, penalty, frame check -- is computed
+//     redundantly by the G lanes (same issue slots as one lane).
+#pragma once
+#include <cstdint>
+
+#include "philox.cuh"
+#include "vehicle.cuh"
+
+namespace bss {
+
+enum CtrlMode { CTRL_PHILOX = 0, CTRL_EPS = 1, CTRL_GIVEN = 2 };
+
+struct RollParams {
+  VehDev V;
+  TrackDev tr;
+  int k_count, k_begin, T, M;
+  int ctrl_mode;      // CtrlMode
+  int noise_on;       // process noise nonzero (dynamics.py:571 skips the add otherwise)
+  int shield;         // det kinds: 1 = smppi
+  float invM, invMm1;
+  float q[8];
+  float v_goal, c_obs, term, beta1 /* 1 - beta */, c_pen, nu;
+  float gamma, prec[4], sfac[4], lo[2], hi[2];
+  float F[9];          // process-noise factor
+  int chol_rank;       // max Cholesky rank: min(4, M - 1) (cov0: 4)
+  uint32_t kc0, kc1;   // control-noise key
+  uint32_t kb0, kb1;   // belief-noise key
+  const float *x0;     // [8]
+  const float *cov0;   // [16]
+  const float *plan;   // [T*2] nominal
+  const double *eps_in;  // [k_count*T*2] (CTRL_EPS / CTRL_GIVEN)
+  const double *u_in;    // [k_count*T*2] (CTRL_GIVEN)
+  const float *z_in;     // [T*k_count*M*7] oracle-noise mode
+  float *u_out;          // [k_count*T*2] clamped controls for the update
+  float *cost_out;       // [k_count]
+  float *mom_out;        // [T*k_count*18] or null
+};
+
+__device__ __forceinline__ float stage_cost(const float x[8], const RollParams &P) {
+  // controllers.py:215-220: sum q_i (x_i - g_i)^2 + C_obs [|e_y| > w]
+  float acc = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float d = (i == 0) ? x[0] - P.v_goal : x[i];
+    acc = fmaf(P.q[i] * d, d, acc);
+  }
+  return acc + ((fabsf(x[6]) > P.tr.half_width) ? P.c_obs : 0.f);
+}
+
+__device__ __forceinline__ float dcbf(float ey, float sigy, const RollParams &P) {
+  // constraints.py:130-137
+  const float margin = fmaxf(P.tr.half_width - P.nu * sigy, 0.f);
+  return margin * margin - ey * ey;
+}
+
+__device__ __forceinline__ float shield_penalty(float hc, float hp, const RollParams &P) {
+  // constraints.py:172-186: C max(-(h_k - (1 - beta) h_{k-1}), 0)
+  return P.c_pen * fmaxf(-(hc - P.beta1 * hp), 0.f);
+}
+
+// Per-(k,t) control: sample/clamp/control-cost (controllers.py:166-177, 223-228).
+__device__ __forceinline__ void control_at(const RollParams &P, int k, int kg, int t,
+                                           float &u0, float &u1, float &ccost) {
+  const float v0 = P.plan[2 * t], v1 = P.plan[2 * t + 1];
+  float e0, e1;
+  if (P.ctrl_mode == CTRL_PHILOX) {
+    float z0, z1;
+    control_normals(P.kc0, P.kc1, (uint32_t)t, (uint32_t)kg, z0, z1);
+    e0 = P.sfac[0] * z0 + P.sfac[1] * z1;
+    e1 = P.sfac[2] * z0 + P.sfac[3] * z1;
+  } else {
+    const size_t o = ((size_t)k * P.T + t) * 2;
+    e0 = (float)P.eps_in[o];
+    e1 = (float)P.eps_in[o + 1];
+  }
+  if (P.ctrl_mode == CTRL_GIVEN) {
+    const size_t o = ((size_t)k * P.T + t) * 2;
+    u0 = (float)P.u_in[o];
+    u1 = (float)P.u_in[o + 1];
+  } else {
+    u0 = fminf(fmaxf(v0 + e0, P.lo[0]), P.hi[0]);
+    u1 = fminf(fmaxf(v1 + e1, P.lo[1]), P.hi[1]);
+  }
+  // gamma * v^T P (v + eps) with the UNCLAMPED v + eps (controllers.py:227)
+  const float a0 = v0 + e0, a1 = v1 + e1;
+  ccost = P.gamma * (v0 * (P.prec[0] * a0 + P.prec[1] * a1) + v1 * (P.prec[2] * a0 + P.prec[3] * a1));
+}
+
+// 4x4 PSD Cholesky with zero-pivot columns left zero (belief.py:235-256).
+// A column is dropped when its pivot is not positive -- exact for the
+// structurally zero rows (noise-free components, zero initial covariance),
+// like the reference's 1e-300 clamp -- and, because a sample covariance of
+// M particles has rank <= M - 1, at most M - 1 pivots are kept (for M <= 4
+// the FP64 reference's extra pivots are rounding noise of O(1e-8 sigma)).
+__device__ __forceinline__ void chol4(const float C[10], float L[10], int max_rank) {
+  // packed lower: L00 L10 L11 L20 L21 L22 L30 L31 L32 L33
+  // C packed upper: c00 c01 c02 c03 c11 c12 c13 c22 c23 c33
+  const float c00 = C[0], c01 = C[1], c02 = C[2], c03 = C[3], c11 = C[4], c12 = C[5],
+              c13 = C[6], c22 = C[7], c23 = C[8], c33 = C[9];
+  int rank = 0;
+  float l00 = 0.f, l10 = 0.f, l20 = 0.f, l30 = 0.f;
+  if (c00 > 0.f && rank < max_rank) {
+    ++rank;
+    l00 = sqrtf(c00);
+    const float inv = 1.f / l00;
+    l10 = c01 * inv; l20 = c02 * inv; l30 = c03 * inv;
+  }
+  float l11 = 0.f, l21 = 0.f, l31 = 0.f;
+  {
+    const float acc = c11 - l10 * l10;
+    if (acc > 0.f && rank < max_rank) {
+      ++rank;
+      l11 = sqrtf(acc);
+      const float inv = 1.f / l11;
+      l21 = (c12 - l20 * l10) * inv;
+      l31 = (c13 - l30 * l10) * inv;
+    }
+  }
+  float l22 = 0.f, l32 = 0.f;
+  {
+    const float acc = c22 - l20 * l20 - l21 * l21;
+    if (acc > 0.f && rank < max_rank) {
+      ++rank;
+      l22 = sqrtf(acc);
+      l32 = (c23 - l30 * l20 - l31 * l21) / l22;
+    }
+  }
+  float l33 = 0.f;
+  {
+    const float acc = c33 - l30 * l30 - l31 * l31 - l32 * l32;
+    if (acc > 0.f && rank < max_rank) l33 = sqrtf(acc);
+  }
+  L[0] = l00; L[1] = l10; L[2] = l11; L[3] = l20; L[4] = l21;
+  L[5] = l22; L[6] = l30; L[7] = l31; L[8] = l32; L[9] = l33;
+}
+
+// Reduce-scatter butterfly of 18 partial sums over a G-lane group, then an
+// all-gather through shared memory; every lane returns the 18 group sums.
+template <int G>
+__device__ __forceinline__ void group_allreduce18(float a[18], int li, float *slot) {
+  // Each level halves the values a lane holds; `base` is the absolute index
+  // of a[0] and `cnt` how many of the held values are real (the rest are
+  // zero padding that must not be written back).
+  int base = 0, cnt = 18;
+#define BSS_RS_LEVEL(N, OFF)                                                   \
+  if (G > OFF) {                                                               \
+    constexpr int H = (N + 1) / 2;                                             \
+    const bool up = (li & OFF) != 0;                                           \
+    _Pragma("unroll") for (int i = 0; i < H; ++i) {                            \
+      const float lo = a[i];                                                   \
+      const float hi = (i + H < N) ? a[i + H] : 0.f;                           \
+      const float send = up ? lo : hi;                                         \
+      const float keep = up ? hi : lo;                                         \
+      a[i] = keep + __shfl_xor_sync(0xffffffffu, send, OFF);                   \
+    }                                                                          \
+    base += up ? H : 0;                                                        \
+    cnt = up ? max(cnt - H, 0) : min(cnt, H);                                  \
+  }
+  // offsets descend from G/2 to 1; level sizes for 18 values: 9, 5, 3, 2, 1
+  if (G == 32) {
+    BSS_RS_LEVEL(18, 16) BSS_RS_LEVEL(9, 8) BSS_RS_LEVEL(5, 4) BSS_RS_LEVEL(3, 2) BSS_RS_LEVEL(2, 1)
+    if (cnt > 0) slot[base] = a[0];
+  } else if (G == 16) {
+    BSS_RS_LEVEL(18, 8) BSS_RS_LEVEL(9, 4) BSS_RS_LEVEL(5, 2) BSS_RS_LEVEL(3, 1)
+#pragma unroll
+    for (int i = 0; i < 2; ++i) if (i < cnt) slot[base + i] = a[i];
+  } else if (G == 8) {
+    BSS_RS_LEVEL(18, 4) BSS_RS_LEVEL(9, 2) BSS_RS_LEVEL(5, 1)
+#pragma unroll
+    for (int i = 0; i < 3; ++i) if (i < cnt) slot[base + i] = a[i];
+  } else if (G == 4) {
+    BSS_RS_LEVEL(18, 2) BSS_RS_LEVEL(9, 1)
+#pragma unroll
+    for (int i = 0; i < 5; ++i) if (i < cnt) slot[base + i] = a[i];
+  } else {  // G == 2
+    BSS_RS_LEVEL(18, 1)
+#pragma unroll
+    for (int i = 0; i < 9; ++i) if (i < cnt) slot[base + i] = a[i];
+  }
+#undef BSS_RS_LEVEL
+  __syncwarp();
+  const float4 *s4 = reinterpret_cast<const float4 *>(slot);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float4 v = s4[i];
+    a[4 * i] = v.x; a[4 * i + 1] = v.y; a[4 * i + 2] = v.z; a[4 * i + 3] = v.w;
+  }
+  const float2 v = reinterpret_cast<const float2 *>(slot)[8];
+  a[16] = v.x;
+  a[17] = v.y;
+}
+
+constexpr int kSlotFloats = 20;   // 18 sums, 16-byte aligned slot
+constexpr int kBlockThreads = 128;
+
+// BSS rollouts.  G: lanes per rollout; PERSIST: keep the particle cloud in
+// shared memory instead of re-projecting (controllers.py:288-305);
+// ZARR: read the reference's normals instead of Philox.
+template <int G, bool PERSIST, bool ZARR>
+__global__ void __launch_bounds__(kBlockThreads) bss_rollout_kernel(const RollParams P) {
+  extern __shared__ float4 smem4[];
+  float *smem = reinterpret_cast<float *>(smem4);
+  constexpr int GPW = 32 / G;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gi = lane / G, li = lane % G;
+  const int warp_global = blockIdx.x * (kBlockThreads / 32) + warp;
+  if (warp_global * GPW >= P.k_count) return;            // whole warp idle
+  const int kraw = warp_global * GPW + gi;
+  const bool active = kraw < P.k_count;
+  const int k = active ? kraw : P.k_count - 1;            // keep shuffles convergent
+  const int kg = P.k_begin + k;
+  float *slots = smem + (warp * GPW + gi) * 2 * kSlotFloats;
+  float *cloud = PERSIST ? smem + (kBlockThreads / 32) * GPW * 2 * kSlotFloats +
+                               (size_t)(warp * GPW + gi) * 8 * P.M
+                         : nullptr;
+  const int M = P.M;
+
+  float mean[8], C[10], L[10];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) mean[i] = P.x0[i];
+  {
+    const int ui[10] = {0, 1, 2, 3, 5, 6, 7, 10, 11, 15};
+#pragma unroll
+    for (int i = 0; i < 10; ++i) C[i] = P.cov0[ui[i]];
+  }
+  chol4(C, L, 4);   // the initial belief covariance is not a sample estimate
+  float h_cur = dcbf(mean[6], sqrtf(fmaxf(C[9], 0.f)), P);
+  float h_prev = h_cur;
+  float total = 0.f;
+  bool dead = false;
+
+  for (int t = 0; t < P.T; ++t) {
+    total += stage_cost(mean, P);
+    if (t > 0) total += shield_penalty(h_cur, h_prev, P);
+    float u0, u1, cc;
+    control_at(P, k, kg, t, u0, u1, cc);
+    total += cc;
+    if (active && li == 0) {
+      reinterpret_cast<float2 *>(P.u_out)[(size_t)k * P.T + t] = make_float2(u0, u1);
+    }
+    const CtlDev ctl = make_ctl(u0, u1, P.V);
+    // shift: the noise-free particle
+    float c[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) c[i] = mean[i];
+    vehicle_step(c, ctl, P.V, P.tr);
+
+    float acc[18];
+#pragma unroll
+    for (int i = 0; i < 18; ++i) acc[i] = 0.f;
+    for (int m = li; m < M; m += G) {
+      float z[7];
+      if (ZARR) {
+        const float *zp = P.z_in + (((size_t)t * P.k_count + k) * M + m) * 7;
+#pragma unroll
+        for (int j = 0; j < 7; ++j) z[j] = zp[j];
+      } else {
+        belief_normals(P.kb0, P.kb1, (uint32_t)t, (uint32_t)kg, (uint32_t)m, z);
+      }
+      float x[8];
+      if (PERSIST && t > 0) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = cloud[i * M + m];
+      } else {
+        // x = mu, tracked subset (vy, r, e_psi, e_y) += L z[0:4] (belief.py:259-272)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = mean[i];
+        x[1] += L[0] * z[0];
+        x[2] += L[1] * z[0] + L[2] * z[1];
+        x[5] += L[3] * z[0] + L[4] * z[1] + L[5] * z[2];
+        x[6] += L[6] * z[0] + L[7] * z[1] + L[8] * z[2] + L[9] * z[3];
+      }
+      vehicle_step(x, ctl, P.V, P.tr);       // per-particle ok is discarded (belief.py:370)
+      if (P.noise_on) {                      // added after integration (dynamics.py:571-572)
+        x[0] += P.F[0] * z[4] + P.F[1] * z[5] + P.F[2] * z[6];
+        x[1] += P.F[3] * z[4] + P.F[4] * z[5] + P.F[5] * z[6];
+        x[2] += P.F[6] * z[4] + P.F[7] * z[5] + P.F[8] * z[6];
+      }
+      if (PERSIST) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) cloud[i * M + m] = x[i];
+      }
+      float d[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        d[i] = x[i] - c[i];
+        acc[i] += d[i];
+      }
+      const float a1 = d[1], a2 = d[2], a5 = d[5], a6 = d[6];
+      acc[8] = fmaf(a1, a1, acc[8]);   acc[9] = fmaf(a1, a2, acc[9]);
+      acc[10] = fmaf(a1, a5, acc[10]); acc[11] = fmaf(a1, a6, acc[11]);
+      acc[12] = fmaf(a2, a2, acc[12]); acc[13] = fmaf(a2, a5, acc[13]);
+      acc[14] = fmaf(a2, a6, acc[14]); acc[15] = fmaf(a5, a5, acc[15]);
+      acc[16] = fmaf(a5, a6, acc[16]); acc[17] = fmaf(a6, a6, acc[17]);
+    }
+    group_allreduce18<G>(acc, li, slots + (t & 1) * kSlotFloats);
+
+    // moments (belief.py:275-308 semantics)
+    float mu[8], dm[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      dm[i] = acc[i] * P.invM;
+      mu[i] = c[i] + dm[i];
+    }
+    {
+      const int sub[4] = {1, 2, 5, 6};
+      int q = 0;
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = a; b < 4; ++b, ++q)
+          C[q] = (acc[8 + q] - acc[sub[a]] * dm[sub[b]]) * P.invMm1;
+    }
+    if (P.mom_out != nullptr && active && li == 0) {
+      float *mo = P.mom_out + ((size_t)t * P.k_count + k) * 18;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mo[i] = mu[i];
+#pragma unroll
+      for (int i = 0; i < 10; ++i) mo[8 + i] = C[i];
+    }
+    // ok = finite(mean) & finite(cov) & 1 - kappa(s_bar) e_bar > 0 (belief.py:376-379)
+    bool fin = true;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) fin &= isfinite(mu[i]);
+#pragma unroll
+    for (int i = 0; i < 10; ++i) fin &= isfinite(C[i]);
+    const float kap = curvature(P.tr, mu[7]);
+    const bool ok = fin && (1.f - kap * mu[6] > 0.f);
+    dead |= !ok;
+    // _finite_or_zero (controllers.py:231-235, 311-312)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) mean[i] = isfinite(mu[i]) ? mu[i] : 0.f;
+#pragma unroll
+    for (int i = 0; i < 10; ++i) C[i] = isfinite(C[i]) ? C[i] : 0.f;
+    h_prev = h_cur;
+    h_cur = dcbf(mean[6], sqrtf(fmaxf(C[9], 0.f)), P);
+    if (!PERSIST) chol4(C, L, P.chol_rank);
+  }
+  total += P.term * stage_cost(mean, P) + shield_penalty(h_cur, h_prev, P);
+  if (active && li == 0) P.cost_out[k] = dead ? __int_as_float(0x7f800000) : total;
+}
+
+// Deterministic rollouts for kind "mppi" / "smppi" (controllers.py:320-338):
+// one lane per k, state carried in registers.
+template <bool SHIELD>
+__global__ void __launch_bounds__(kBlockThreads) det_rollout_kernel(const RollParams P) {
+  const int k = blockIdx.x * kBlockThreads + threadIdx.x;
+  if (k >= P.k_count) return;
+  const int kg = P.k_begin + k;
+  float x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = P.x0[i];
+  float h_cur = SHIELD ? dcbf(x[6], 0.f, P) : 0.f;
+  float h_prev = h_cur;
+  float total = 0.f;
+  bool dead = false;
+  for (int t = 0; t < P.T; ++t) {
+    total += stage_cost(x, P);
+    if (SHIELD && t > 0) total += shield_penalty(h_cur, h_prev, P);
+    float u0, u1, cc;
+    control_at(P, k, kg, t, u0, u1, cc);
+    total += cc;
+    reinterpret_cast<float2 *>(P.u_out)[(size_t)k * P.T + t] = make_float2(u0, u1);
+    const bool ok = vehicle_step(x, make_ctl(u0, u1, P.V), P.V, P.tr);
+    dead |= !ok;
+    if (SHIELD) {
+      h_prev = h_cur;
+      h_cur = dcbf(x[6], 0.f, P);
+    }
+  }
+  total += P.term * stage_cost(x, P);
+  if (SHIELD) total += shield_penalty(h_cur, h_prev, P);
+  P.cost_out[k] = dead ? __int_as_float(0x7f800000) : total;
+}
+
+// step_array (dynamics.py:550-573): one particle per thread, FP64 I/O.
+__global__ void step_array_kernel(VehDev V, TrackDev tr, int n, const double *x, const double *u,
+                                  const double *w, double *xo, uint8_t *oko) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float s[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s[j] = (float)x[(size_t)i * 8 + j];
+  const bool ok = vehicle_step(s, make_ctl((float)u[2 * (size_t)i], (float)u[2 * (size_t)i + 1], V), V, tr);
+  if (w != nullptr) {
+#pragma unroll
+    for (int j = 0; j < 3; ++j) s[j] += (float)w[(size_t)i * 3 + j];
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) xo[(size_t)i * 8 + j] = (double)s[j];
+  oko[i] = ok ? 1 : 0;
+}
+
+}  // namespace bss

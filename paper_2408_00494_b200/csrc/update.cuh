@@ -1,0 +1,167 @@
+// Information-theoretic update (controllers.py:180-194):
+//   w_k = exp(-(S_k - min_finite S) / lambda),  v+ = clip(sum_k w_k u_k / sum_k w_k)
+// as a two-level, fixed-order (deterministic) reduction in FP64:
+//   1. update_partials_kernel: each block owns a contiguous k-chunk and emits
+//      a record {beta_b, Z_b, Z2_b, n_b, argmin_b, N_b[2T]} with weights
+//      relative to its OWN minimum beta_b (one pass over u, no global min);
+//   2. combine_kernel: rescales records by exp(-(beta_b - beta)/lambda) and
+//      sums them in record order.  The same kernel combines K-shard records
+//      of several GPUs after one NCCL all-reduce, so a
+//      sharded iteration equals the single-GPU one up to FP64 rounding.
+#pragma once
+#include <cstdint>
+
+namespace bss {
+
+constexpr int kRecHead = 5;   // beta, Z, Z2, n_finite, argmin
+constexpr int kUpdThreads = 256;
+
+__device__ __forceinline__ double to_d(float v) { return (double)v; }
+__device__ __forceinline__ double to_d(double v) { return v; }
+
+template <typename CT, typename UT>
+__global__ void __launch_bounds__(kUpdThreads)
+update_partials_kernel(int n, int k_begin, int T2, const CT *costs, const UT *u, double lam,
+                       int chunk, double *rec) {
+  __shared__ double s_min[kUpdThreads];
+  __shared__ long long s_arg[kUpdThreads];
+  __shared__ double s_cnt[kUpdThreads];
+  __shared__ double s_w[kUpdThreads];
+  __shared__ double s_z[kUpdThreads], s_z2[kUpdThreads];
+  const int tid = threadIdx.x;
+  const int k0 = blockIdx.x * chunk;
+  const int k1 = min(n, k0 + chunk);
+  double *out = rec + (size_t)blockIdx.x * (kRecHead + T2);
+  // pass 1: block min over finite costs (ties -> smallest k), finite count
+  double mn = __longlong_as_double(0x7ff0000000000000ll);
+  long long arg = -1;
+  double cnt = 0.0;
+  for (int k = k0 + tid; k < k1; k += kUpdThreads) {
+    const double c = to_d(costs[k]);
+    if (isfinite(c)) {
+      cnt += 1.0;
+      if (c < mn) { mn = c; arg = k; }
+    }
+  }
+  s_min[tid] = mn; s_arg[tid] = arg; s_cnt[tid] = cnt;
+  __syncthreads();
+  for (int s = kUpdThreads / 2; s > 0; s >>= 1) {
+    if (tid < s) {
+      const double a = s_min[tid], b = s_min[tid + s];
+      const long long ia = s_arg[tid], ib = s_arg[tid + s];
+      if (b < a || (b == a && ib >= 0 && (ia < 0 || ib < ia))) { s_min[tid] = b; s_arg[tid] = ib; }
+      s_cnt[tid] += s_cnt[tid + s];
+    }
+    __syncthreads();
+  }
+  const double beta = s_min[0];
+  const bool any = s_cnt[0] > 0.0;
+  // pass 2: weights relative to beta_b, fixed-order sums
+  double z = 0.0, z2 = 0.0;
+  double nacc[4] = {0.0, 0.0, 0.0, 0.0};   // columns tid, tid+256, ... (2T <= 1024)
+  for (int base = k0; base < k1; base += kUpdThreads) {
+    __syncthreads();
+    const int k = base + tid;
+    double w = 0.0;
+    if (k < k1 && any) {
+      const double c = to_d(costs[k]);
+      w = isfinite(c) ? exp(-(c - beta) / lam) : 0.0;
+    }
+    s_w[tid] = w;
+    z += w;
+    z2 += w * w;
+    __syncthreads();
+    const int cnt_k = min(kUpdThreads, k1 - base);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int col = tid + j * kUpdThreads;
+      if (col < T2) {
+        double a = nacc[j];
+        for (int i = 0; i < cnt_k; ++i) a = fma(s_w[i], to_d(u[(size_t)(base + i) * T2 + col]), a);
+        nacc[j] = a;
+      }
+    }
+  }
+  s_z[tid] = z;
+  s_z2[tid] = z2;
+  __syncthreads();
+  for (int s = kUpdThreads / 2; s > 0; s >>= 1) {
+    if (tid < s) { s_z[tid] += s_z[tid + s]; s_z2[tid] += s_z2[tid + s]; }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    out[0] = beta;
+    out[1] = s_z[0];
+    out[2] = s_z2[0];
+    out[3] = s_cnt[0];
+    out[4] = (double)(s_arg[0] < 0 ? -1 : s_arg[0] + k_begin);
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int col = tid + j * kUpdThreads;
+    if (col < T2) out[kRecHead + col] = nacc[j];
+  }
+}
+
+// Combine `nrec` records.  final == 0: write one record to rec_out.
+// final == 1: v+ = clip(N/Z) -> vplus (double), warm-start shifted plan
+// (ControlPlan.shifted, controllers.py:154-156) -> plan_out (float, may be
+// null), head {beta, Z, Z2, n, argmin} -> head_out.
+__global__ void __launch_bounds__(kUpdThreads)
+combine_kernel(int nrec, int T2, const double *rec, double lam, int final_, double *rec_out,
+               double lo0, double lo1, double hi0, double hi1, double *vplus, float *plan_out,
+               double *head_out) {
+  __shared__ double s_scale[1024];
+  __shared__ double s_head[kRecHead];
+  const int tid = threadIdx.x;
+  const int R = kRecHead + T2;
+  if (tid == 0) {
+    double beta = __longlong_as_double(0x7ff0000000000000ll), arg = -1.0, n = 0.0;
+    for (int r = 0; r < nrec; ++r) {
+      const double *h = rec + (size_t)r * R;
+      if (h[3] > 0.0) {
+        n += h[3];
+        if (h[0] < beta || (h[0] == beta && (arg < 0.0 || h[4] < arg))) { beta = h[0]; arg = h[4]; }
+      }
+    }
+    double z = 0.0, z2 = 0.0;
+    for (int r = 0; r < nrec; ++r) {
+      const double *h = rec + (size_t)r * R;
+      double sc = 0.0;
+      if (h[3] > 0.0) sc = exp(-(h[0] - beta) / lam);
+      if (r < 1024) s_scale[r] = sc;
+      z += sc * h[1];
+      z2 += sc * sc * h[2];
+    }
+    s_head[0] = beta; s_head[1] = z; s_head[2] = z2; s_head[3] = n; s_head[4] = arg;
+  }
+  __syncthreads();
+  for (int col = tid; col < T2; col += kUpdThreads) {
+    double a = 0.0;
+    for (int r = 0; r < nrec; ++r) {
+      const double sc = (r < 1024) ? s_scale[r] : 0.0;
+      if (sc != 0.0) a = fma(sc, rec[(size_t)r * R + kRecHead + col], a);
+    }
+    if (!final_) {
+      rec_out[kRecHead + col] = a;
+    } else {
+      const double v = a / s_head[1];
+      const double l = (col & 1) ? lo1 : lo0, h = (col & 1) ? hi1 : hi0;
+      vplus[col] = fmin(fmax(v, l), h);
+    }
+  }
+  if (tid < kRecHead) {
+    if (!final_) rec_out[tid] = s_head[tid];
+    else head_out[tid] = s_head[tid];
+  }
+  if (final_ && plan_out != nullptr) {
+    __syncthreads();
+    __threadfence_block();
+    for (int col = tid; col < T2; col += kUpdThreads) {
+      const int src = (col + 2 < T2) ? col + 2 : col;   // drop first, repeat last
+      plan_out[col] = (float)vplus[src];
+    }
+  }
+}
+
+}  // namespace bss

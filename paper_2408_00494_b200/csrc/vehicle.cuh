@@ -1,0 +1,176 @@
+// FP32 single-track Pacejka model in the road-aligned frame, one particle
+// per call, all state in registers.
+//
+// Restates the reference numba kernels (belief_mppi/dynamics.py):
+//   curvature()    <- _curv_scalar   dynamics.py:340-369
+//   vehicle_step() <- _tire_row      dynamics.py:372-395
+//                   + _derivs_row    dynamics.py:398-437
+//                   + _step_kernel   dynamics.py:447-497 (Euler branch)
+// Deliberate FP32 restatements (checked by the parity tests):
+//   * the friction-ellipse factor sqrt(max(1 - (Fx/D)^2, 0)) is |cos theta|
+//     of the same magic-formula angle (identical algebra, no cancellation);
+//   * sin/cos of the steering angle and drive_gain*throttle are hoisted per
+//     (k, t) because all M particles of a rollout share the control;
+//   * kappa(s) uses a uniform cell index + one-step correction instead of a
+//     binary search (same piecewise-linear interpolant, incl. the closing
+//     segment [s_{n-1}, L) -> kappa_0).
+#pragma once
+#include <cstdint>
+
+#include "fastmath.cuh"
+
+namespace bss {
+
+struct VehDev {
+  float inv_m, inv_iz, lf, lr, R, inv_jw;
+  float Byf, Cyf, Byr, Cyr, Bxf, Cxf, Bxr, Cxr;
+  float Dxf, Dyf, Dxr, Dyr;
+  float drive, vfloor, rrf, rrr, spin_scale, dt;
+  int mf_poly;   // all magic-formula C <= 1.3: angles fit sin_mf/cos_mf's range
+};
+
+// node[j] = {s_j, kappa_j, slope_j, s_{j+1}} plus a sentinel node[n].
+struct TrackDev {
+  const float4 *node;
+  const int *cell;
+  float L, inv_h, half_width;
+  int ncell, n, closed;
+};
+
+struct CtlDev {
+  float delta, cd, sd, drive_u1;
+};
+
+// Python/numba floor-mod (dynamics.py:486-489): result in [0, L], with
+// (-tiny) % L == L.  Exact for x in [-L, 2L) (Sterbenz), fmodf otherwise.
+__device__ __forceinline__ float floor_mod(float x, float L) {
+  if (x >= 0.f && x < L) return x;
+  if (x >= L && x < 2.f * L) return x - L;
+  if (x < 0.f && x >= -L) return x + L;
+  float r = fmodf(x, L);
+  if (r < 0.f) r += L;
+  return r;
+}
+
+// pi - ((pi - a) mod 2pi) (dynamics.py:486).  Inside (-pi, pi] this is the
+// identity (to 1e-16 in the FP64 reference); evaluating it literally in FP32
+// would quantise every heading error to ulp(pi) = 2.4e-7 rad, so the
+// formula is applied only when a wrap actually happens.
+__device__ __forceinline__ float wrap_pi(float a) {
+  const float PI = 3.14159265358979f, TWO_PI = 6.28318530717959f;
+  if (a > -PI && a <= PI) return a;
+  return PI - floor_mod(PI - a, TWO_PI);
+}
+
+__device__ __forceinline__ float curvature(const TrackDev &tr, float s) {
+  const float sw = tr.closed ? floor_mod(s, tr.L) : fminf(fmaxf(s, 0.f), tr.L);
+  int ci = __float2int_rz(sw * tr.inv_h);
+  ci = min(max(ci, 0), tr.ncell - 1);
+  int lo = __ldg(tr.cell + ci);
+  float4 nd = __ldg(tr.node + lo);
+  if (sw < nd.x) {
+    nd = __ldg(tr.node + lo - 1);
+  } else if (sw >= nd.w) {
+    nd = __ldg(tr.node + lo + 1);
+  }
+  return fmaf(nd.z, sw - nd.x, nd.y);
+}
+
+__device__ __forceinline__ bool all_finite8(const float x[8]) {
+  bool ok = true;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) ok &= isfinite(x[i]);
+  return ok;
+}
+
+// One Euler step x <- x + dt f(x, u), wraps, non-finite -> 0.  Returns the
+// reference's per-particle ok (frame > 0 and finite).
+__device__ __forceinline__ bool vehicle_step(float x[8], const CtlDev &c, const VehDev &V,
+                                             const TrackDev &tr) {
+  const float vx = x[0], vy = x[1], r = x[2], wf = x[3], wr = x[4], ep = x[5], ey = x[6],
+              s = x[7];
+  // _tire_row: low-speed floor keeps the sign of vx.
+  const float vxe = (vx >= 0.f) ? fmaxf(vx, V.vfloor) : fminf(vx, -V.vfloor);
+#ifdef BSS_EXACT_MATH
+  const float inv_den = 1.0f / fabsf(vxe);
+  const float af = c.delta - atan2f(vy + V.lf * r, vxe);
+  const float ar = -atan2f(vy - V.lr * r, vxe);
+#else
+  const float rx = __frcp_rn(vxe);          // |vxe| >= v_floor > 0
+  const float inv_den = fabsf(rx);
+  const float af = c.delta - atan2_rcp(vy + V.lf * r, vxe, rx);
+  const float ar = -atan2_rcp(vy - V.lr * r, vxe, rx);
+#endif
+  const float sgf = (wf * V.R - vx) * inv_den;
+  const float sgr = (wr * V.R - vx) * inv_den;
+  const float tyf = V.Cyf * atanf(V.Byf * af), tyr = V.Cyr * atanf(V.Byr * ar);
+  const float txf = V.Cxf * atanf(V.Bxf * sgf), txr = V.Cxr * atanf(V.Bxr * sgr);
+  float syf, syr, sxf, cxf, sxr, cxr;
+#ifndef BSS_EXACT_MATH
+  if (V.mf_poly) {
+    syf = sin_mf(tyf); syr = sin_mf(tyr);
+    sxf = sin_mf(txf); cxf = cos_mf(txf);
+    sxr = sin_mf(txr); cxr = cos_mf(txr);
+  } else
+#endif
+  {
+    syf = sinf(tyf); syr = sinf(tyr);
+    sincosf(txf, &sxf, &cxf);
+    sincosf(txr, &sxr, &cxr);
+  }
+  const float fxf = V.Dxf * sxf, fxr = V.Dxr * sxr;
+  const float fyf = V.Dyf * syf * fabsf(cxf), fyr = V.Dyr * syr * fabsf(cxr);
+  // _derivs_row
+  const float fxb = fxf * c.cd - fyf * c.sd;
+  const float fyb = fxf * c.sd + fyf * c.cd;
+  const float dvx = (fxb + fxr) * V.inv_m + vy * r;
+  const float dvy = (fyb + fyr) * V.inv_m - vx * r;
+  const float dr = (V.lf * fyb - V.lr * fyr) * V.inv_iz;
+#ifdef BSS_EXACT_MATH
+  const float spf = tanhf(wf * V.spin_scale), spr = tanhf(wr * V.spin_scale);
+#else
+  const float spf = tanh_sat(wf * V.spin_scale), spr = tanh_sat(wr * V.spin_scale);
+#endif
+  const float dwf = (-V.R * fxf - V.rrf * spf) * V.inv_jw;
+  const float dwr = (c.drive_u1 - V.R * fxr - V.rrr * spr) * V.inv_jw;
+  const float kap = curvature(tr, s);
+  float frame = 1.f - kap * ey;
+  bool ok = frame > 0.f;
+  if (frame < 1e-3f) frame = 1e-3f;
+  float se, ce;
+#ifdef BSS_EXACT_MATH
+  sincosf(ep, &se, &ce);
+  const float ds = (vx * ce - vy * se) / frame;
+#else
+  sincos_pi(ep, se, ce);
+  const float ds = __fdividef(vx * ce - vy * se, frame);   // frame in [1e-3, 1 + kappa w]
+#endif
+  const float dey = vx * se + vy * ce;
+  const float dep = r - kap * ds;
+  // _step_kernel Euler branch + wraps
+  x[0] = vx + V.dt * dvx;
+  x[1] = vy + V.dt * dvy;
+  x[2] = r + V.dt * dr;
+  x[3] = wf + V.dt * dwf;
+  x[4] = wr + V.dt * dwr;
+  x[5] = wrap_pi(ep + V.dt * dep);
+  x[6] = ey + V.dt * dey;
+  const float s1 = s + V.dt * ds;
+  x[7] = tr.closed ? floor_mod(s1, tr.L) : fminf(fmaxf(s1, 0.f), tr.L);
+  if (!all_finite8(x)) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = isfinite(x[i]) ? x[i] : 0.f;
+    ok = false;
+  }
+  return ok;
+}
+
+__device__ __forceinline__ CtlDev make_ctl(float delta, float throttle, const VehDev &V) {
+  CtlDev c;
+  c.delta = delta;
+  sincosf(delta, &c.sd, &c.cd);
+  c.drive_u1 = V.drive * throttle;
+  return c;
+}
+
+}  // namespace bss

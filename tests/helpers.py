@@ -1,0 +1,82 @@
+"""Shared test helpers: load golden fixtures, rebuild their inputs with this
+repo's host mirror, and run the CPU oracle on them."""
+
+import json
+import types
+from pathlib import Path
+
+import numpy as np
+
+from cases import build, case_by_name
+
+from paper_2408_00494_b200 import controllers as mc
+from paper_2408_00494_b200 import dynamics as md
+
+GOLDEN = Path(__file__).resolve().parent / "golden"
+
+MINE = types.SimpleNamespace(
+    VehicleParams=md.VehicleParams, VehicleState=md.VehicleState, NoiseModel=md.NoiseModel,
+    CostSpec=mc.CostSpec, MppiConfig=mc.MppiConfig, make_test_track=md.make_test_track,
+    with_timestep=md.with_timestep)
+
+
+def load_golden(name):
+    d = np.load(GOLDEN / f"{name}.npz")
+    meta = json.loads(str(d["meta"]))
+    return meta, {k: d[k] for k in d.files if k != "meta"}
+
+
+class Inputs:
+    """Everything the captured iteration of a golden case consumed."""
+
+    def __init__(self, name):
+        from oracle import bss_oracle as orc
+
+        self.meta, self.gold = load_golden(name)
+        case = self.case = case_by_name(name)
+        (self.cfg, self.cost, self.model, self.track, self.noise, self.x0, self.cov0,
+         _) = build(case, MINE)
+        self.K, self.T, self.M = case["K"], case["T"], case["M"]
+        self.kind = case["kind"]
+        self.plan = self.gold["plan_before"]
+        self.iteration = self.meta["iteration"]
+        lo = np.array([-self.cfg.bounds.delta_max, self.cfg.bounds.throttle_min])
+        hi = np.array([self.cfg.bounds.delta_max, self.cfg.bounds.throttle_max])
+        self.lo, self.hi = lo, hi
+        factor = md.psd_factor(self.cfg.sigma_eps)
+        self.u, self.eps, self.z = orc.control_step_inputs(
+            case["seed"], case["run_path"], self.iteration, self.K, self.T, max(self.M, 2),
+            self.plan, factor, lo, hi, kind=self.kind)
+        self.ctx = mc.RolloutContext(self.model, self.track, self.cost, noise=self.noise)
+        self.prob = orc.Problem.from_reference(self.ctx)
+
+    def oracle(self, record=None):
+        from oracle import bss_oracle as orc
+
+        if self.kind == "bss":
+            costs = orc.rollout_bss(self.prob, self.x0, self.cov0, self.u, self.eps, self.plan,
+                                    self.z, self.cfg.precision, self.cfg.control_cost_weight,
+                                    persist=self.case["persist"], record=record)
+        else:
+            costs = orc.rollout_det(self.prob, self.kind, self.x0, self.u, self.eps, self.plan,
+                                    self.cfg.precision, self.cfg.control_cost_weight)
+        vplus = None
+        if np.isfinite(costs).any():
+            vplus = orc.mppi_update(costs, self.u, self.cfg.temperature, self.lo, self.hi)
+        return costs, vplus
+
+
+def moments_rel_err(mean_a, cov_a, mean_b, cov_b):
+    """SURVEY.md 8c moment metric: |dmu_i| / max(|mu_i|, sigma_i) over the
+    tracked components (sigma from b) and |dSigma_ab| / sqrt(S_aa S_bb)."""
+    sub = [1, 2, 5, 6]
+    sig = np.sqrt(np.clip(np.diagonal(cov_b, axis1=-2, axis2=-1), 0, None))
+    scale_m = np.abs(mean_b).copy()
+    scale_m[..., sub] = np.maximum(scale_m[..., sub], sig)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        em = np.abs(mean_a - mean_b) / scale_m
+        em = np.where(scale_m == 0, np.where(mean_a == mean_b, 0.0, np.inf), em)
+        denom = np.sqrt(np.einsum("...i,...j->...ij", sig ** 2, sig ** 2))
+        ec = np.abs(cov_a - cov_b) / denom
+        ec = np.where(denom == 0, np.where(cov_a == cov_b, 0.0, np.inf), ec)
+    return float(np.max(em)), float(np.max(ec))

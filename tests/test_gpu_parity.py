@@ -1,0 +1,135 @@
+"""GPU parity: the sm_100a path (through the C ABI) vs the CPU oracle on the
+same inputs and the reference's own noise (oracle-noise mode).
+
+Tolerances (north_star):
+  * rollout costs: 1e-3 relative for every rollout with non-negligible
+    weight (S - min S <= 100 lambda); the fraction of ALL rollouts within
+    1e-3 is asserted separately (off-track rollouts diverge chaotically);
+  * belief moments: |dmu_i| <= 1e-4 max(|mu_i|, sigma_i) and
+    |dSigma_ab| <= 1e-4 sqrt(S_aa S_bb), exact zeros stay zero;
+  * v+: 1e-4 absolute unless the oracle's best two costs are a near-tie.
+"""
+
+import numpy as np
+import pytest
+
+from cases import CASES, UPDATE_BATCHES, update_batch
+from helpers import GOLDEN, Inputs, moments_rel_err
+
+from paper_2408_00494_b200 import controllers as mc
+
+pytestmark = pytest.mark.gpu
+
+BSS = [c["name"] for c in CASES if c["kind"] == "bss"]
+ALL = [c["name"] for c in CASES]
+COST_RTOL = 1e-3
+MOM_TOL = 1e-4
+VPLUS_ATOL = 1e-4
+
+
+def _weighted(costs, lam):
+    fin = np.isfinite(costs)
+    out = np.zeros_like(fin)
+    if fin.any():
+        out = fin & (costs - costs[fin].min() <= 100.0 * lam)
+    return out
+
+
+def _near_tie(costs, lam, cost_err=1e-5):
+    fin = np.sort(costs[np.isfinite(costs)])
+    return fin.size > 1 and (fin[1] - fin[0]) < 10 * cost_err * abs(fin[0]) + 1e-9
+
+
+def _gpu_rollout(inp, moments=False):
+    batch = mc.RolloutBatch(inp.u, inp.eps)
+    if inp.kind == "bss":
+        class _Z:
+            def standard_normal(self, shape):
+                assert shape == inp.z.shape
+                return inp.z
+        return mc.rollout_bss(inp.x0, inp.cov0, batch, inp.plan, inp.ctx, _Z(), inp.M,
+                              precision=inp.cfg.precision, cost_weight=inp.cfg.control_cost_weight,
+                              persist_particles=inp.case["persist"], moments=moments)
+    fn = mc.rollout_smppi if inp.kind == "smppi" else mc.rollout_mppi
+    return fn(inp.x0, batch, inp.plan, inp.ctx, precision=inp.cfg.precision,
+              cost_weight=inp.cfg.control_cost_weight)
+
+
+@pytest.mark.parametrize("name", ALL)
+def test_rollout_costs(name):
+    inp = Inputs(name)
+    ref = inp.gold["costs"]
+    got = _gpu_rollout(inp)
+    fin = np.isfinite(ref)
+    assert np.array_equal(np.isfinite(got), fin), "dead-rollout pattern differs"
+    rel = np.abs(got[fin] - ref[fin]) / np.abs(ref[fin])
+    w = _weighted(ref, inp.cfg.temperature)
+    print(f"{name}: max rel err weighted {rel[w[fin]].max() if w.any() else 0:.2e}, "
+          f"all {rel.max() if rel.size else 0:.2e}, frac<1e-3 {np.mean(rel < COST_RTOL) if rel.size else 1:.4f}")
+    if w.any():
+        assert rel[w[fin]].max() <= COST_RTOL
+    if rel.size:
+        assert np.mean(rel < COST_RTOL) >= 0.99
+
+
+@pytest.mark.parametrize("name", BSS)
+def test_belief_moments(name):
+    inp = Inputs(name)
+    costs, mom = _gpu_rollout(inp, moments=True)
+    gold = inp.gold
+    ks = gold["ks"]
+    mean = mom[:, ks, :8].astype(np.float64)
+    up = mom[:, ks, 8:].astype(np.float64)
+    cov = np.empty(mean.shape[:2] + (4, 4))
+    q = 0
+    for a in range(4):
+        for b in range(a, 4):
+            cov[..., a, b] = cov[..., b, a] = up[..., q]
+            q += 1
+    # compare rollouts that survive the horizon (a dead rollout is +inf and
+    # weightless; its moments after leaving the curvilinear frame are
+    # frame-singular in both implementations)
+    alive = np.broadcast_to(np.isfinite(gold["costs"][ks])[None, :], mean.shape[:2])
+    em, ec = moments_rel_err(mean[alive], cov[alive], gold["means"][alive], gold["covs"][alive])
+    zero = gold["covs"][alive] == 0.0
+    print(f"{name}: moments mean {em:.2e} cov {ec:.2e}")
+    assert em <= MOM_TOL and ec <= MOM_TOL
+    assert np.all(cov[alive][zero] == 0.0), "exact zero covariances must stay zero"
+
+
+@pytest.mark.parametrize("name", ALL)
+def test_control_step_oracle_noise(name):
+    """Controller.control_step in oracle-noise mode reproduces v+ / u0 /
+    next plan of the reference iteration."""
+    inp = Inputs(name)
+    ctrl = mc.Controller(inp.cfg, inp.cost, inp.model, inp.track, noise=inp.noise,
+                         seed=inp.case["seed"], run_path=inp.case["run_path"],
+                         noise_source="reference")
+    ctrl.plan = mc.ControlPlan(inp.plan.copy())
+    ctrl.iteration = inp.iteration
+    if inp.meta["invalid"]:
+        with pytest.raises(mc.AllRolloutsInvalid):
+            ctrl.control_step(inp.x0, inp.cov0)
+        assert ctrl.iteration == inp.iteration
+        return
+    u0, nxt = ctrl.control_step(inp.x0, inp.cov0)
+    gold = inp.gold
+    d = ctrl.last_diagnostics
+    err = np.abs(d["vplus"] - gold["vplus"]).max()
+    print(f"{name}: |dv+| {err:.2e} ess {d['ess']:.3f} argmin {d['cost_argmin']} "
+          f"ref argmin {int(np.argmin(gold['costs']))}")
+    if not _near_tie(gold["costs"], inp.cfg.temperature):
+        assert err <= VPLUS_ATOL
+        assert d["cost_argmin"] == int(np.argmin(gold["costs"]))
+    np.testing.assert_allclose(u0, gold["u0"], atol=VPLUS_ATOL)
+    np.testing.assert_allclose(nxt.controls, gold["plan_after"], atol=VPLUS_ATOL)
+    assert ctrl.iteration == inp.iteration + 1
+
+
+@pytest.mark.parametrize("j", range(len(UPDATE_BATCHES)))
+def test_update_law_golden(j):
+    d = np.load(GOLDEN / "update_law.npz")
+    costs, controls, lam = update_batch(j)
+    plan = mc.mppi_update(mc.RolloutBatch(controls, np.zeros_like(controls), costs), lam,
+                          mc.ControlBounds())
+    np.testing.assert_allclose(plan.controls, d[f"u{j}_vplus"], rtol=0, atol=1e-12)
