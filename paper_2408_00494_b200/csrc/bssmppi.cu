@@ -63,6 +63,7 @@ struct bssmppi_ctx {
   int *d_cell = nullptr;
   float *d_state = nullptr;   // x0[8] | cov0[16] | plan[2T]
   float *d_u = nullptr, *d_cost = nullptr;
+  float4 *d_ctl = nullptr;    // per-(k,t) control table
   double *d_eps = nullptr, *d_uin = nullptr;
   float *d_z = nullptr, *d_mom = nullptr;
   size_t cap_eps = 0, cap_uin = 0, cap_z = 0, cap_mom = 0;
@@ -277,6 +278,7 @@ RollParams iteration_params(bssmppi_ctx *c, const uint32_t *kc, const uint32_t *
   rp.cov0 = c->d_state + 8;
   rp.plan = c->d_state + 24;
   rp.u_out = c->d_u;
+  rp.ctl = c->d_ctl;
   rp.cost_out = c->d_cost;
   rp.mom_out = nullptr;
   rp.eps_in = nullptr;
@@ -382,6 +384,7 @@ int bssmppi_create(const bssmppi_problem *problem, int32_t device, bssmppi_ctx *
   if ((rc = dev_alloc(&c->d_state, 24 + T2))) return bail(rc);
   if ((rc = dev_alloc(&c->d_u, (size_t)c->k_count * T2))) return bail(rc);
   if ((rc = dev_alloc(&c->d_cost, c->k_count))) return bail(rc);
+  if ((rc = dev_alloc(&c->d_ctl, (size_t)c->k_count * c->T))) return bail(rc);
   if ((rc = dev_alloc(&c->d_rec, (size_t)c->nblocks * (kRecHead + T2)))) return bail(rc);
   if ((rc = dev_alloc(&c->d_out, T2 + kRecHead))) return bail(rc);
   if (cudaMallocHost((void **)&c->h_state, (24 + T2) * sizeof(float)) != cudaSuccess ||
@@ -399,7 +402,7 @@ void bssmppi_destroy(bssmppi_ctx *c) {
   DeviceGuard guard(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   cudaFree(c->d_node); cudaFree(c->d_cell); cudaFree(c->d_state); cudaFree(c->d_u);
-  cudaFree(c->d_cost); cudaFree(c->d_eps); cudaFree(c->d_uin); cudaFree(c->d_z);
+  cudaFree(c->d_cost); cudaFree(c->d_ctl); cudaFree(c->d_eps); cudaFree(c->d_uin); cudaFree(c->d_z);
   cudaFree(c->d_mom); cudaFree(c->d_rec); cudaFree(c->d_out);
   if (c->h_state) cudaFreeHost(c->h_state);
   if (c->h_out) cudaFreeHost(c->h_out);

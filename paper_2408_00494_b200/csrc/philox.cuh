@@ -14,19 +14,26 @@ struct Philox4 {
   uint32_t x, y, z, w;
 };
 
-__host__ __device__ __forceinline__ uint32_t mulhi32(uint32_t a, uint32_t b) {
+// 32x32 -> 64 multiply in one IMAD.WIDE.U32 on the device.
+__host__ __device__ __forceinline__ void mulhilo32(uint32_t a, uint32_t b, uint32_t &hi, uint32_t &lo) {
 #ifdef __CUDA_ARCH__
-  return __umulhi(a, b);
+  uint64_t p;
+  asm("mul.wide.u32 %0, %1, %2;" : "=l"(p) : "r"(a), "r"(b));
+  lo = (uint32_t)p;
+  hi = (uint32_t)(p >> 32);
 #else
-  return (uint32_t)(((uint64_t)a * (uint64_t)b) >> 32);
+  const uint64_t p = (uint64_t)a * (uint64_t)b;
+  lo = (uint32_t)p;
+  hi = (uint32_t)(p >> 32);
 #endif
 }
 
 __host__ __device__ __forceinline__ Philox4 philox4x32_10(Philox4 c, uint32_t k0, uint32_t k1) {
 #pragma unroll
   for (int i = 0; i < 10; ++i) {
-    const uint32_t hi0 = mulhi32(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
-    const uint32_t hi1 = mulhi32(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    uint32_t hi0, lo0, hi1, lo1;
+    mulhilo32(0xD2511F53u, c.x, hi0, lo0);
+    mulhilo32(0xCD9E8D57u, c.z, hi1, lo1);
     c = Philox4{hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0};
     k0 += 0x9E3779B9u;
     k1 += 0xBB67AE85u;
@@ -53,6 +60,14 @@ __device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float &z0, fl
   z1 = r * s;
 }
 
+// Single normal (cosine branch) of a Box-Muller pair.
+__device__ __forceinline__ void box_muller1(uint32_t a, uint32_t b, float &z0) {
+  const float u1 = 2.0f - __uint_as_float(0x3f800000u | (a >> 9));
+  const float u2 = __uint_as_float(0x3f800000u | (b >> 9)) - 1.5f;
+  const float r = sqrt_approx(-1.38629436112f * __log2f(u1));
+  z0 = r * __cosf(6.28318530718f * u2);
+}
+
 // The 7 standard normals of particle-step (t, k, m): [0:4] re-projection
 // on the tracked subset, [4:7] process noise -- the column layout of the
 // reference's z_all block (controllers.py:285-287, belief.py:328-333).
@@ -60,11 +75,10 @@ __device__ __forceinline__ void belief_normals(uint32_t k0, uint32_t k1, uint32_
                                                uint32_t m, float z[7]) {
   const Philox4 a = philox4x32_10(Philox4{t, m, kg, 0u}, k0, k1);
   const Philox4 b = philox4x32_10(Philox4{t, m, kg, 1u}, k0, k1);
-  float spare;
   box_muller(a.x, a.y, z[0], z[1]);
   box_muller(a.z, a.w, z[2], z[3]);
   box_muller(b.x, b.y, z[4], z[5]);
-  box_muller(b.z, b.w, z[6], spare);
+  box_muller1(b.z, b.w, z[6]);
 }
 
 // The 2 standard normals of control sample (k, t) (controllers.py:175).

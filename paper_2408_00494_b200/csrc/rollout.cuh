@@ -53,6 +53,7 @@ struct RollParams {
   const double *u_in;    // [k_count*T*2] (CTRL_GIVEN)
   const float *z_in;     // [T*k_count*M*7] oracle-noise mode
   float *u_out;          // [k_count*T*2] clamped controls for the update
+  float4 *ctl;           // [k_count*T] per-(k,t) control table {delta, cos, sin, drive*u1}
   float *cost_out;       // [k_count]
   float *mom_out;        // [T*k_count*18] or null
 };
@@ -214,6 +215,94 @@ __device__ __forceinline__ void group_allreduce18(float a[18], int li, float *sl
 constexpr int kSlotFloats = 20;   // 18 sums, 16-byte aligned slot
 constexpr int kBlockThreads = 128;
 
+// Group-wide sum over G lanes (xor butterfly; every lane gets the total).
+template <int G>
+__device__ __forceinline__ float group_sum(float v) {
+#pragma unroll
+  for (int off = G / 2; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
+
+// Prologue shared by the rollout kernels: the G lanes of a group sample the
+// T controls of rollout k in parallel (lane l takes t = l, l+G, ...),
+// write the clamped u for the update and the per-(k,t) control table
+// {delta, cos delta, sin delta, drive_gain * throttle} the particle steps
+// read, and return the rollout's control cost (controllers.py:166-177,
+// 223-228) summed over the group.
+template <int G>
+__device__ __forceinline__ float control_prologue(const RollParams &P, int k, int kg, int li,
+                                                  bool active) {
+  float cc = 0.f;
+  for (int t = li; t < P.T; t += G) {
+    float u0, u1, c;
+    control_at(P, k, kg, t, u0, u1, c);
+    cc += c;
+    if (active) {
+      const size_t o = (size_t)k * P.T + t;
+      reinterpret_cast<float2 *>(P.u_out)[o] = make_float2(u0, u1);
+      float sd, cd;
+      sincosf(u0, &sd, &cd);
+      P.ctl[o] = make_float4(u0, cd, sd, P.V.drive * u1);
+    }
+  }
+  __syncwarp();
+  return group_sum<G>(cc);
+}
+
+// One particle-step: re-project (or load the persistent particle), Euler
+// step, process noise.  Returns the post-step state in x.
+template <bool PERSIST, bool ZARR>
+__device__ __forceinline__ void particle_step(const RollParams &P, int t, int k, int kg, int m,
+                                              const float mean[8], const float L[10],
+                                              const CtlDev &ctl, float *cloud, float x[8]) {
+  const int M = P.M;
+  float z[7];
+  if (ZARR) {
+    const float *zp = P.z_in + (((size_t)t * P.k_count + k) * M + m) * 7;
+#pragma unroll
+    for (int j = 0; j < 7; ++j) z[j] = zp[j];
+  } else {
+    belief_normals(P.kb0, P.kb1, (uint32_t)t, (uint32_t)kg, (uint32_t)m, z);
+  }
+  if (PERSIST && t > 0) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = cloud[i * M + m];
+  } else {
+    // x = mu, tracked subset (vy, r, e_psi, e_y) += L z[0:4] (belief.py:259-272)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = mean[i];
+    x[1] += L[0] * z[0];
+    x[2] += L[1] * z[0] + L[2] * z[1];
+    x[5] += L[3] * z[0] + L[4] * z[1] + L[5] * z[2];
+    x[6] += L[6] * z[0] + L[7] * z[1] + L[8] * z[2] + L[9] * z[3];
+  }
+  vehicle_step(x, ctl, P.V, P.tr);       // per-particle ok is discarded (belief.py:370)
+  if (P.noise_on) {                      // added after integration (dynamics.py:571-572)
+    x[0] += P.F[0] * z[4] + P.F[1] * z[5] + P.F[2] * z[6];
+    x[1] += P.F[3] * z[4] + P.F[4] * z[5] + P.F[5] * z[6];
+    x[2] += P.F[6] * z[4] + P.F[7] * z[5] + P.F[8] * z[6];
+  }
+  if (PERSIST) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) cloud[i * M + m] = x[i];
+  }
+}
+
+__device__ __forceinline__ void accumulate(float acc[18], const float x[8], const float c[8]) {
+  float d[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    d[i] = x[i] - c[i];
+    acc[i] += d[i];
+  }
+  const float a1 = d[1], a2 = d[2], a5 = d[5], a6 = d[6];
+  acc[8] = fmaf(a1, a1, acc[8]);   acc[9] = fmaf(a1, a2, acc[9]);
+  acc[10] = fmaf(a1, a5, acc[10]); acc[11] = fmaf(a1, a6, acc[11]);
+  acc[12] = fmaf(a2, a2, acc[12]); acc[13] = fmaf(a2, a5, acc[13]);
+  acc[14] = fmaf(a2, a6, acc[14]); acc[15] = fmaf(a5, a5, acc[15]);
+  acc[16] = fmaf(a5, a6, acc[16]); acc[17] = fmaf(a6, a6, acc[17]);
+}
+
 // BSS rollouts.  G: lanes per rollout; PERSIST: keep the particle cloud in
 // shared memory instead of re-projecting (controllers.py:288-305);
 // ZARR: read the reference's normals instead of Philox.
@@ -235,7 +324,9 @@ __global__ void __launch_bounds__(kBlockThreads) bss_rollout_kernel(const RollPa
                                (size_t)(warp * GPW + gi) * 8 * P.M
                          : nullptr;
   const int M = P.M;
+  const bool has0 = li < M;                              // lane owns particle m = li
 
+  float total = control_prologue<G>(P, k, kg, li, active);
   float mean[8], C[10], L[10];
 #pragma unroll
   for (int i = 0; i < 8; ++i) mean[i] = P.x0[i];
@@ -247,72 +338,28 @@ __global__ void __launch_bounds__(kBlockThreads) bss_rollout_kernel(const RollPa
   chol4(C, L, 4);   // the initial belief covariance is not a sample estimate
   float h_cur = dcbf(mean[6], sqrtf(fmaxf(C[9], 0.f)), P);
   float h_prev = h_cur;
-  float total = 0.f;
   bool dead = false;
+  const float4 *ctl_row = P.ctl + (size_t)k * P.T;
 
   for (int t = 0; t < P.T; ++t) {
     total += stage_cost(mean, P);
     if (t > 0) total += shield_penalty(h_cur, h_prev, P);
-    float u0, u1, cc;
-    control_at(P, k, kg, t, u0, u1, cc);
-    total += cc;
-    if (active && li == 0) {
-      reinterpret_cast<float2 *>(P.u_out)[(size_t)k * P.T + t] = make_float2(u0, u1);
-    }
-    const CtlDev ctl = make_ctl(u0, u1, P.V);
-    // shift: the noise-free particle
-    float c[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) c[i] = mean[i];
-    vehicle_step(c, ctl, P.V, P.tr);
+    const float4 cv = ctl_row[t];
+    const CtlDev ctl{cv.x, cv.y, cv.z, cv.w};
 
+    // Particle 0 of the group doubles as the shift of the one-pass moments:
+    // it sits O(sigma) from the mean, and a zero-spread cloud gives d == 0.
     float acc[18];
 #pragma unroll
     for (int i = 0; i < 18; ++i) acc[i] = 0.f;
-    for (int m = li; m < M; m += G) {
-      float z[7];
-      if (ZARR) {
-        const float *zp = P.z_in + (((size_t)t * P.k_count + k) * M + m) * 7;
+    float x[8], c[8];
+    if (has0) particle_step<PERSIST, ZARR>(P, t, k, kg, li, mean, L, ctl, cloud, x);
 #pragma unroll
-        for (int j = 0; j < 7; ++j) z[j] = zp[j];
-      } else {
-        belief_normals(P.kb0, P.kb1, (uint32_t)t, (uint32_t)kg, (uint32_t)m, z);
-      }
-      float x[8];
-      if (PERSIST && t > 0) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) x[i] = cloud[i * M + m];
-      } else {
-        // x = mu, tracked subset (vy, r, e_psi, e_y) += L z[0:4] (belief.py:259-272)
-#pragma unroll
-        for (int i = 0; i < 8; ++i) x[i] = mean[i];
-        x[1] += L[0] * z[0];
-        x[2] += L[1] * z[0] + L[2] * z[1];
-        x[5] += L[3] * z[0] + L[4] * z[1] + L[5] * z[2];
-        x[6] += L[6] * z[0] + L[7] * z[1] + L[8] * z[2] + L[9] * z[3];
-      }
-      vehicle_step(x, ctl, P.V, P.tr);       // per-particle ok is discarded (belief.py:370)
-      if (P.noise_on) {                      // added after integration (dynamics.py:571-572)
-        x[0] += P.F[0] * z[4] + P.F[1] * z[5] + P.F[2] * z[6];
-        x[1] += P.F[3] * z[4] + P.F[4] * z[5] + P.F[5] * z[6];
-        x[2] += P.F[6] * z[4] + P.F[7] * z[5] + P.F[8] * z[6];
-      }
-      if (PERSIST) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) cloud[i * M + m] = x[i];
-      }
-      float d[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        d[i] = x[i] - c[i];
-        acc[i] += d[i];
-      }
-      const float a1 = d[1], a2 = d[2], a5 = d[5], a6 = d[6];
-      acc[8] = fmaf(a1, a1, acc[8]);   acc[9] = fmaf(a1, a2, acc[9]);
-      acc[10] = fmaf(a1, a5, acc[10]); acc[11] = fmaf(a1, a6, acc[11]);
-      acc[12] = fmaf(a2, a2, acc[12]); acc[13] = fmaf(a2, a5, acc[13]);
-      acc[14] = fmaf(a2, a6, acc[14]); acc[15] = fmaf(a5, a5, acc[15]);
-      acc[16] = fmaf(a5, a6, acc[16]); acc[17] = fmaf(a6, a6, acc[17]);
+    for (int i = 0; i < 8; ++i) c[i] = __shfl_sync(0xffffffffu, x[i], 0, G);
+    if (has0) accumulate(acc, x, c);
+    for (int m = li + G; m < M; m += G) {
+      particle_step<PERSIST, ZARR>(P, t, k, kg, m, mean, L, ctl, cloud, x);
+      accumulate(acc, x, c);
     }
     group_allreduce18<G>(acc, li, slots + (t & 1) * kSlotFloats);
 

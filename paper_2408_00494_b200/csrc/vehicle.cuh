@@ -76,11 +76,11 @@ __device__ __forceinline__ float curvature(const TrackDev &tr, float s) {
   return fmaf(nd.z, sw - nd.x, nd.y);
 }
 
+// Fast screen: a sum of finite values is finite unless it overflows (then
+// the caller's per-component slow path decides); inf/NaN always propagate.
 __device__ __forceinline__ bool all_finite8(const float x[8]) {
-  bool ok = true;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) ok &= isfinite(x[i]);
-  return ok;
+  const float s = ((x[0] + x[1]) + (x[2] + x[3])) + ((x[4] + x[5]) + (x[6] + x[7]));
+  return fabsf(s) < __int_as_float(0x7f800000);
 }
 
 // One Euler step x <- x + dt f(x, u), wraps, non-finite -> 0.  Returns the
@@ -158,9 +158,13 @@ __device__ __forceinline__ bool vehicle_step(float x[8], const CtlDev &c, const 
   const float s1 = s + V.dt * ds;
   x[7] = tr.closed ? floor_mod(s1, tr.L) : fminf(fmaxf(s1, 0.f), tr.L);
   if (!all_finite8(x)) {
+    bool fin = true;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) x[i] = isfinite(x[i]) ? x[i] : 0.f;
-    ok = false;
+    for (int i = 0; i < 8; ++i) {
+      fin &= isfinite(x[i]);
+      x[i] = isfinite(x[i]) ? x[i] : 0.f;
+    }
+    ok = ok && fin;
   }
   return ok;
 }

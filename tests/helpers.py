@@ -69,6 +69,8 @@ class Inputs:
 def moments_rel_err(mean_a, cov_a, mean_b, cov_b):
     """SURVEY.md 8c moment metric: |dmu_i| / max(|mu_i|, sigma_i) over the
     tracked components (sigma from b) and |dSigma_ab| / sqrt(S_aa S_bb)."""
+    if mean_a.size == 0:
+        return 0.0, 0.0
     sub = [1, 2, 5, 6]
     sig = np.sqrt(np.clip(np.diagonal(cov_b, axis1=-2, axis2=-1), 0, None))
     scale_m = np.abs(mean_b).copy()
