@@ -96,6 +96,7 @@ typedef struct bssmppi_diag {
   double weight_sum;        /* sum_k exp(-(S_k - min S)/lambda) */
   double ess;               /* (sum w)^2 / sum w^2 */
   float device_ms;          /* CUDA-event time of the last enqueued iteration */
+  float rollout_ms;         /* ... of which the fused rollout kernel */
 } bssmppi_diag;
 
 typedef struct bssmppi_ctx bssmppi_ctx;
@@ -140,6 +141,12 @@ int bssmppi_upload_state(bssmppi_ctx *ctx, const double *x0, const double *cov0,
                          const double *plan);
 int bssmppi_enqueue_iteration(bssmppi_ctx *ctx, const uint32_t key_ctrl[2],
                               const uint32_t key_belief[2]);
+/* Device-resident K-shard iteration: partial record into partials_dev[slot]
+ * (asynchronous), and the asynchronous combine of nslots records into v+
+ * with the warm-start shift of the device plan. */
+int bssmppi_enqueue_partials(bssmppi_ctx *ctx, const uint32_t key_ctrl[2],
+                             const uint32_t key_belief[2], double *partials_dev, int32_t slot);
+int bssmppi_enqueue_combine(bssmppi_ctx *ctx, const double *partials_dev, int32_t nslots);
 /* Synchronise and read the last iteration's v+ (nullable) and diagnostics. */
 int bssmppi_download(bssmppi_ctx *ctx, double *vplus, bssmppi_diag *diag);
 
@@ -174,6 +181,9 @@ int bssmppi_step_array(bssmppi_ctx *ctx, int32_t n, const double *x, const doubl
 int bssmppi_philox4x32(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
 int bssmppi_belief_normals(const uint32_t key[2], int32_t t, int32_t k, int32_t m_count,
                            float *out /* m_count*7 */);
+
+/* Measured FP32 FFMA throughput of the device (roofline denominator). */
+int bssmppi_ffma_peak(int32_t device, double *tflops);
 
 #ifdef __cplusplus
 }

@@ -352,3 +352,37 @@ def control_step_inputs(seed, run_path, iteration, K, T, M, nominal, sigma_facto
     u, eps = sample_controls(nominal, sigma_factor, z_ctrl, lo, hi)
     z_all = sub(*rp, 3, iteration).standard_normal((T, K, M, 7)) if kind == "bss" else None
     return u, eps, z_all
+
+
+def shard_record(costs, u, lam, k_begin=0):
+    """Partial update record of one K-shard, restating csrc/update.cuh on the
+    host (test infrastructure): {beta, Z, Z2, n_finite, argmin, N[2T]} with
+    weights relative to the shard's own minimum."""
+    costs = np.asarray(costs, float)
+    T2 = u.shape[1] * 2
+    rec = np.zeros(5 + T2)
+    fin = np.isfinite(costs)
+    rec[0] = costs[fin].min() if fin.any() else np.inf
+    rec[3] = fin.sum()
+    rec[4] = (k_begin + int(np.argmin(np.where(fin, costs, np.inf)))) if fin.any() else -1
+    if fin.any():
+        w = np.where(fin, np.exp(-(costs - rec[0]) / lam), 0.0)
+        rec[1] = w.sum()
+        rec[2] = (w * w).sum()
+        rec[5:] = np.einsum("k,ki->i", w, u.reshape(len(costs), T2))
+    return rec
+
+
+def combine_records(recs, lam, lo, hi):
+    """Rank-order combine of shard records -> clamp(v+) (csrc/update.cuh
+    combine_kernel); equals mppi_update on the concatenated batch."""
+    recs = np.asarray(recs, float)
+    live = recs[:, 3] > 0
+    if not live.any():
+        raise RuntimeError("AllRolloutsInvalid")
+    beta = recs[live, 0].min()
+    sc = np.where(live, np.exp(-(recs[:, 0] - beta) / lam), 0.0)
+    Z = (sc * recs[:, 1]).sum()
+    N = (sc[:, None] * recs[:, 5:]).sum(0)
+    v = (N / Z).reshape(-1, 2)
+    return np.clip(v, lo, hi)

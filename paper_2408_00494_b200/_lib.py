@@ -47,7 +47,8 @@ class Problem(C.Structure):
 
 class Diag(C.Structure):
     _fields_ = [("cost_min", C.c_double), ("cost_argmin", C.c_int64), ("n_finite", C.c_int64),
-                ("weight_sum", C.c_double), ("ess", C.c_double), ("device_ms", C.c_float)]
+                ("weight_sum", C.c_double), ("ess", C.c_double), ("device_ms", C.c_float),
+                ("rollout_ms", C.c_float)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -75,6 +76,8 @@ SIGNATURES = {
     "bssmppi_upload_state": (C.c_int, [_ctx, _dp, _dp, _dp]),
     "bssmppi_enqueue_iteration": (C.c_int, [_ctx, _u32p, _u32p]),
     "bssmppi_download": (C.c_int, [_ctx, _dp, C.POINTER(Diag)]),
+    "bssmppi_enqueue_partials": (C.c_int, [_ctx, _u32p, _u32p, C.c_void_p, C.c_int32]),
+    "bssmppi_enqueue_combine": (C.c_int, [_ctx, C.c_void_p, C.c_int32]),
     "bssmppi_rollout": (C.c_int, [_ctx, _dp, _dp, _dp, _dp, _dp, _fp, _u32p, _dp, _fp]),
     "bssmppi_mppi_update": (C.c_int, [C.c_int32, C.c_int32, _dp, _dp, C.c_double, _dp, _dp, _dp,
                                       C.POINTER(Diag)]),
@@ -83,6 +86,7 @@ SIGNATURES = {
     "bssmppi_step_array": (C.c_int, [_ctx, C.c_int32, _dp, _dp, _dp, _dp, _u8p]),
     "bssmppi_philox4x32": (C.c_int, [_u32p, _u32p, _u32p]),
     "bssmppi_belief_normals": (C.c_int, [_u32p, C.c_int32, C.c_int32, C.c_int32, _fp]),
+    "bssmppi_ffma_peak": (C.c_int, [C.c_int32, _dp]),
 }
 
 _LIB = None

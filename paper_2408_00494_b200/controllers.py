@@ -428,12 +428,16 @@ class Controller:
             z = np.ascontiguousarray(zb[:, k0:k0 + kn], dtype=np.float32)
         return eps, z
 
-    def _inputs(self, state, cov):
+    def _inputs_state(self, state, cov):
         x0 = np.ascontiguousarray(state, dtype=np.float64).reshape(8)
         cov0 = None if cov is None else np.ascontiguousarray(cov, dtype=np.float64).reshape(16)
         plan = np.ascontiguousarray(self.plan.controls, dtype=np.float64)
         if plan.shape != (self.config.horizon, CONTROL_DIM):
             raise ValueError("plan shape does not match the horizon")
+        return x0, cov0, plan
+
+    def _inputs(self, state, cov):
+        x0, cov0, plan = self._inputs_state(state, cov)
         if self.noise_source == "reference":
             eps, z = self._noise_arrays()
             kc = kb = None
@@ -460,6 +464,27 @@ class Controller:
                                              kb, _lib.dptr(eps), _lib.fptr(z), _lib.dptr(vplus),
                                              _lib.C.byref(diag)))
         return self._finish(vplus, diag)
+
+    # -- device-resident loop (throughput measurement; bench.py) ----------
+    def upload_state(self, state, cov=None):
+        """Stage x0 / cov0 / the current plan on the device."""
+        dev = self._device_ctx()
+        x0, cov0, plan, *_ = self._inputs_state(state, cov)
+        _lib.check(dev.lib.bssmppi_upload_state(dev.h, _lib.dptr(x0), _lib.dptr(cov0), _lib.dptr(plan)))
+
+    def enqueue_iteration(self, key_ctrl, key_belief):
+        """Asynchronous iteration on the device-resident state; the device
+        plan is warm-start shifted in place."""
+        dev = self._device_ctx()
+        _lib.check(dev.lib.bssmppi_enqueue_iteration(dev.h, _lib.key_arr(key_ctrl), _lib.key_arr(key_belief)))
+
+    def download(self):
+        """Synchronise; (v+ (T,2), diagnostics dict) of the last iteration."""
+        dev = self._device_ctx()
+        vplus = np.empty((self.config.horizon, CONTROL_DIM))
+        diag = _lib.Diag()
+        _status(dev.lib.bssmppi_download(dev.h, _lib.dptr(vplus), _lib.C.byref(diag)))
+        return vplus, diag.as_dict()
 
     def close(self):
         if self._dev is not None:

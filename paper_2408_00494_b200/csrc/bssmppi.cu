@@ -64,6 +64,7 @@ struct bssmppi_ctx {
   float *d_state = nullptr;   // x0[8] | cov0[16] | plan[2T]
   float *d_u = nullptr, *d_cost = nullptr;
   float4 *d_ctl = nullptr;    // per-(k,t) control table
+  float *d_cc = nullptr;      // per-(k,t) control-cost terms
   double *d_eps = nullptr, *d_uin = nullptr;
   float *d_z = nullptr, *d_mom = nullptr;
   size_t cap_eps = 0, cap_uin = 0, cap_z = 0, cap_mom = 0;
@@ -72,7 +73,7 @@ struct bssmppi_ctx {
   double *d_out = nullptr;    // vplus[2T] | head[5]
   float *h_state = nullptr;   // pinned
   double *h_out = nullptr;    // pinned
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, evr = nullptr;   // iteration start/end, rollout end
   bool timed = false;
 };
 
@@ -279,14 +280,15 @@ RollParams iteration_params(bssmppi_ctx *c, const uint32_t *kc, const uint32_t *
   rp.plan = c->d_state + 24;
   rp.u_out = c->d_u;
   rp.ctl = c->d_ctl;
+  rp.ccost = c->d_cc;
   rp.cost_out = c->d_cost;
   rp.mom_out = nullptr;
   rp.eps_in = nullptr;
   rp.u_in = nullptr;
   rp.z_in = nullptr;
   rp.ctrl_mode = CTRL_PHILOX;
-  rp.kc0 = kc ? kc[0] : 0u; rp.kc1 = kc ? kc[1] : 0u;
-  rp.kb0 = kb ? kb[0] : 0u; rp.kb1 = kb ? kb[1] : 0u;
+  rp.kc = philox_schedule(kc ? kc[0] : 0u, kc ? kc[1] : 0u);
+  rp.kb = philox_schedule(kb ? kb[0] : 0u, kb ? kb[1] : 0u);
   return rp;
 }
 
@@ -315,6 +317,7 @@ int run_iteration(bssmppi_ctx *c, RollParams &rp, bool final_, double *rec_out) 
   CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
   int rc = launch_rollout(c, rp, rp.z_in != nullptr);
   if (rc) return rc;
+  CUDA_TRY(cudaEventRecord(c->evr, c->stream));
   rc = launch_update(c, final_, rec_out);
   if (rc) return rc;
   CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
@@ -333,9 +336,13 @@ int finish(bssmppi_ctx *c, double *vplus, bssmppi_diag *diag) {
     diag->ess = head[2] > 0.0 ? head[1] * head[1] / head[2] : 0.0;
     diag->n_finite = (int64_t)head[3];
     diag->cost_argmin = (int64_t)head[4];
-    float ms = 0.f;
-    if (c->timed) cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+    float ms = 0.f, rms = 0.f;
+    if (c->timed) {
+      cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+      cudaEventElapsedTime(&rms, c->ev0, c->evr);
+    }
     diag->device_ms = ms;
+    diag->rollout_ms = rms;
   }
   if (!(head[3] > 0.0)) return fail(BSSMPPI_ERR_ALL_INVALID, "no rollout produced a finite cost");
   if (vplus) std::memcpy(vplus, c->h_out, T2 * sizeof(double));
@@ -385,12 +392,14 @@ int bssmppi_create(const bssmppi_problem *problem, int32_t device, bssmppi_ctx *
   if ((rc = dev_alloc(&c->d_u, (size_t)c->k_count * T2))) return bail(rc);
   if ((rc = dev_alloc(&c->d_cost, c->k_count))) return bail(rc);
   if ((rc = dev_alloc(&c->d_ctl, (size_t)c->k_count * c->T))) return bail(rc);
+  if ((rc = dev_alloc(&c->d_cc, (size_t)c->k_count * c->T))) return bail(rc);
   if ((rc = dev_alloc(&c->d_rec, (size_t)c->nblocks * (kRecHead + T2)))) return bail(rc);
   if ((rc = dev_alloc(&c->d_out, T2 + kRecHead))) return bail(rc);
   if (cudaMallocHost((void **)&c->h_state, (24 + T2) * sizeof(float)) != cudaSuccess ||
       cudaMallocHost((void **)&c->h_out, (T2 + kRecHead) * sizeof(double)) != cudaSuccess)
     return bail(fail(BSSMPPI_ERR_CUDA, "cudaMallocHost failed"));
-  if (cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess)
+  if (cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
+      cudaEventCreate(&c->evr) != cudaSuccess)
     return bail(fail(BSSMPPI_ERR_CUDA, "cudaEventCreate failed"));
   CUDA_TRY(cudaMemset(c->d_state, 0, (24 + T2) * sizeof(float)));
   *out = c;
@@ -402,12 +411,13 @@ void bssmppi_destroy(bssmppi_ctx *c) {
   DeviceGuard guard(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   cudaFree(c->d_node); cudaFree(c->d_cell); cudaFree(c->d_state); cudaFree(c->d_u);
-  cudaFree(c->d_cost); cudaFree(c->d_ctl); cudaFree(c->d_eps); cudaFree(c->d_uin); cudaFree(c->d_z);
+  cudaFree(c->d_cost); cudaFree(c->d_ctl); cudaFree(c->d_cc); cudaFree(c->d_eps); cudaFree(c->d_uin); cudaFree(c->d_z);
   cudaFree(c->d_mom); cudaFree(c->d_rec); cudaFree(c->d_out);
   if (c->h_state) cudaFreeHost(c->h_state);
   if (c->h_out) cudaFreeHost(c->h_out);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->evr) cudaEventDestroy(c->evr);
   delete c;
 }
 
@@ -464,8 +474,16 @@ int bssmppi_step_partials(bssmppi_ctx *c, const double *x0, const double *cov0, 
   return run_iteration(c, rp, false, partials_dev + (size_t)slot * (kRecHead + 2 * c->T));
 }
 
-int bssmppi_update_combine(bssmppi_ctx *c, const double *partials_dev, int32_t nslots, double *vplus,
-                           bssmppi_diag *diag) {
+int bssmppi_enqueue_partials(bssmppi_ctx *c, const uint32_t key_ctrl[2], const uint32_t key_belief[2],
+                             double *partials_dev, int32_t slot) {
+  if (!c) return fail(BSSMPPI_ERR_INVALID, "ctx is NULL");
+  if (!partials_dev || slot < 0) return fail(BSSMPPI_ERR_INVALID, "partials buffer/slot invalid");
+  DeviceGuard guard(c->device);
+  RollParams rp = iteration_params(c, key_ctrl, key_belief);
+  return run_iteration(c, rp, false, partials_dev + (size_t)slot * (kRecHead + 2 * c->T));
+}
+
+int bssmppi_enqueue_combine(bssmppi_ctx *c, const double *partials_dev, int32_t nslots) {
   if (!c) return fail(BSSMPPI_ERR_INVALID, "ctx is NULL");
   if (!partials_dev || nslots < 1 || nslots > 1024) return fail(BSSMPPI_ERR_INVALID, "bad partials / nslots");
   DeviceGuard guard(c->device);
@@ -474,6 +492,14 @@ int bssmppi_update_combine(bssmppi_ctx *c, const double *partials_dev, int32_t n
                                                    c->lo[1], c->hi[0], c->hi[1], c->d_out, c->d_state + 24,
                                                    c->d_out + T2);
   CUDA_TRY(cudaGetLastError());
+  return BSSMPPI_OK;
+}
+
+int bssmppi_update_combine(bssmppi_ctx *c, const double *partials_dev, int32_t nslots, double *vplus,
+                           bssmppi_diag *diag) {
+  int rc = bssmppi_enqueue_combine(c, partials_dev, nslots);
+  if (rc) return rc;
+  DeviceGuard guard(c->device);
   return finish(c, vplus, diag);
 }
 
@@ -546,6 +572,7 @@ int bssmppi_mppi_update(int32_t K, int32_t T, const double *costs, const double 
     diag->n_finite = (int64_t)head[3];
     diag->cost_argmin = (int64_t)head[4];
     diag->device_ms = 0.f;
+    diag->rollout_ms = 0.f;
   }
   if (!(head[3] > 0.0)) return fail(BSSMPPI_ERR_ALL_INVALID, "no rollout produced a finite cost");
   std::memcpy(vplus, h.data(), T2 * sizeof(double));
@@ -570,6 +597,25 @@ __global__ void sample_controls_kernel(int n, int T, const double *z, double f0,
   u[2 * i + 1] = fmin(fmax(nominal[2 * t + 1] + e1, lo1), hi1);
 }
 
+// Measured FP32 peak (roofline denominator): 8 independent FFMA chains per
+// thread, 148 * 8 blocks of 256 threads.
+__global__ void __launch_bounds__(256) ffma_peak_kernel(float *out, int iters, float a, float b) {
+  float x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = threadIdx.x * 1e-3f + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) x[i] = fmaf(x[i], a, b);
+    }
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += x[i];
+  if (s == 12345.678f) out[0] = s;
+}
+
 __global__ void philox_kernel(Philox4 c, uint32_t k0, uint32_t k1, uint32_t *out) {
   const Philox4 r = philox4x32_10(c, k0, k1);
   out[0] = r.x; out[1] = r.y; out[2] = r.z; out[3] = r.w;
@@ -579,7 +625,7 @@ __global__ void belief_normals_kernel(uint32_t k0, uint32_t k1, int t, int k, in
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= mcount) return;
   float z[7];
-  belief_normals(k0, k1, (uint32_t)t, (uint32_t)k, (uint32_t)m, z);
+  belief_normals(philox_schedule(k0, k1), (uint32_t)t, (uint32_t)k, (uint32_t)m, z);
   for (int j = 0; j < 7; ++j) out[(size_t)m * 7 + j] = z[j];
 }
 }  // namespace
@@ -649,6 +695,38 @@ int bssmppi_philox4x32(const uint32_t ctr[4], const uint32_t key[2], uint32_t ou
   if (e == cudaSuccess) e = cudaMemcpy(out, d, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost);
   cudaFree(d);
   if (e != cudaSuccess) return fail(BSSMPPI_ERR_CUDA, "philox: %s", cudaGetErrorString(e));
+  return BSSMPPI_OK;
+}
+
+int bssmppi_ffma_peak(int32_t device, double *tflops) {
+  if (!tflops) return fail(BSSMPPI_ERR_INVALID, "NULL argument");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+    return fail(BSSMPPI_ERR_CUDA, "no CUDA device %d", device);
+  DeviceGuard guard(device);
+  cudaSetDevice(device);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  float *d = nullptr;
+  int rc = dev_alloc(&d, 1);
+  if (rc) return rc;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int blocks = sms * 8, iters = 4096;
+  ffma_peak_kernel<<<blocks, 256>>>(d, 64, 0.999f, 1e-3f);   // warm-up
+  cudaEventRecord(e0);
+  ffma_peak_kernel<<<blocks, 256>>>(d, iters, 0.999f, 1e-3f);
+  cudaEventRecord(e1);
+  cudaError_t e = cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(BSSMPPI_ERR_CUDA, "ffma_peak: %s", cudaGetErrorString(e));
+  const double flops = 2.0 * 8 * 16 * (double)iters * blocks * 256;
+  *tflops = flops / (ms * 1e-3) / 1e12;
   return BSSMPPI_OK;
 }
 

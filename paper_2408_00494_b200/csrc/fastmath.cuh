@@ -70,8 +70,7 @@ __device__ __forceinline__ void sincos_pi(float x, float &s, float &c) {
 // atan(y r) in the right half plane, +-pi shifted in the left one.
 __device__ __forceinline__ float atan2_rcp(float y, float x, float r) {
   const float a = atanf(y * r);
-  if (x >= 0.f) return a;
-  return a + copysignf(3.14159265358979f, y);
+  return x >= 0.f ? a : a + copysignf(3.14159265358979f, y);
 }
 
 // tanh(x); |x| >= 9.02 rounds to +-1 in FP32 (wheels at speed), which skips

@@ -41,6 +41,33 @@ __host__ __device__ __forceinline__ Philox4 philox4x32_10(Philox4 c, uint32_t k0
   return c;
 }
 
+// Round-key schedule k_i = k + i * (W0, W1), i = 0..9, precomputed on the
+// host once per iteration so the rounds read their keys as kernel-constant
+// operands instead of re-deriving them per call.
+struct PhiloxKeys {
+  uint32_t k[20];
+};
+
+__host__ __device__ __forceinline__ PhiloxKeys philox_schedule(uint32_t k0, uint32_t k1) {
+  PhiloxKeys r;
+  for (int i = 0; i < 10; ++i) {
+    r.k[2 * i] = k0 + (uint32_t)i * 0x9E3779B9u;
+    r.k[2 * i + 1] = k1 + (uint32_t)i * 0xBB67AE85u;
+  }
+  return r;
+}
+
+__host__ __device__ __forceinline__ Philox4 philox4x32_10(Philox4 c, const PhiloxKeys &rk) {
+#pragma unroll
+  for (int i = 0; i < 10; ++i) {
+    uint32_t hi0, lo0, hi1, lo1;
+    mulhilo32(0xD2511F53u, c.x, hi0, lo0);
+    mulhilo32(0xCD9E8D57u, c.z, hi1, lo1);
+    c = Philox4{hi1 ^ c.y ^ rk.k[2 * i], lo1, hi0 ^ c.w ^ rk.k[2 * i + 1], lo0};
+  }
+  return c;
+}
+
 #ifdef __CUDACC__
 __device__ __forceinline__ float sqrt_approx(float x) {
   float y;
@@ -71,10 +98,10 @@ __device__ __forceinline__ void box_muller1(uint32_t a, uint32_t b, float &z0) {
 // The 7 standard normals of particle-step (t, k, m): [0:4] re-projection
 // on the tracked subset, [4:7] process noise -- the column layout of the
 // reference's z_all block (controllers.py:285-287, belief.py:328-333).
-__device__ __forceinline__ void belief_normals(uint32_t k0, uint32_t k1, uint32_t t, uint32_t kg,
+__device__ __forceinline__ void belief_normals(const PhiloxKeys &rk, uint32_t t, uint32_t kg,
                                                uint32_t m, float z[7]) {
-  const Philox4 a = philox4x32_10(Philox4{t, m, kg, 0u}, k0, k1);
-  const Philox4 b = philox4x32_10(Philox4{t, m, kg, 1u}, k0, k1);
+  const Philox4 a = philox4x32_10(Philox4{t, m, kg, 0u}, rk);
+  const Philox4 b = philox4x32_10(Philox4{t, m, kg, 1u}, rk);
   box_muller(a.x, a.y, z[0], z[1]);
   box_muller(a.z, a.w, z[2], z[3]);
   box_muller(b.x, b.y, z[4], z[5]);
@@ -82,9 +109,9 @@ __device__ __forceinline__ void belief_normals(uint32_t k0, uint32_t k1, uint32_
 }
 
 // The 2 standard normals of control sample (k, t) (controllers.py:175).
-__device__ __forceinline__ void control_normals(uint32_t k0, uint32_t k1, uint32_t t, uint32_t kg,
+__device__ __forceinline__ void control_normals(const PhiloxKeys &rk, uint32_t t, uint32_t kg,
                                                 float &z0, float &z1) {
-  const Philox4 a = philox4x32_10(Philox4{t, kg, 0x5eedc0deu, 0u}, k0, k1);
+  const Philox4 a = philox4x32_10(Philox4{t, kg, 0x5eedc0deu, 0u}, rk);
   box_muller(a.x, a.y, z0, z1);
 }
 #endif

@@ -44,8 +44,8 @@ struct RollParams {
   float gamma, prec[4], sfac[4], lo[2], hi[2];
   float F[9];          // process-noise factor
   int chol_rank;       // max Cholesky rank: min(4, M - 1) (cov0: 4)
-  uint32_t kc0, kc1;   // control-noise key
-  uint32_t kb0, kb1;   // belief-noise key
+  PhiloxKeys kc;       // control-noise key schedule
+  PhiloxKeys kb;       // belief-noise key schedule
   const float *x0;     // [8]
   const float *cov0;   // [16]
   const float *plan;   // [T*2] nominal
@@ -54,6 +54,7 @@ struct RollParams {
   const float *z_in;     // [T*k_count*M*7] oracle-noise mode
   float *u_out;          // [k_count*T*2] clamped controls for the update
   float4 *ctl;           // [k_count*T] per-(k,t) control table {delta, cos, sin, drive*u1}
+  float *ccost;          // [k_count*T] per-(k,t) control-cost terms
   float *cost_out;       // [k_count]
   float *mom_out;        // [T*k_count*18] or null
 };
@@ -87,7 +88,7 @@ __device__ __forceinline__ void control_at(const RollParams &P, int k, int kg, i
   float e0, e1;
   if (P.ctrl_mode == CTRL_PHILOX) {
     float z0, z1;
-    control_normals(P.kc0, P.kc1, (uint32_t)t, (uint32_t)kg, z0, z1);
+    control_normals(P.kc, (uint32_t)t, (uint32_t)kg, z0, z1);
     e0 = P.sfac[0] * z0 + P.sfac[1] * z1;
     e1 = P.sfac[2] * z0 + P.sfac[3] * z1;
   } else {
@@ -232,21 +233,25 @@ __device__ __forceinline__ float group_sum(float v) {
 template <int G>
 __device__ __forceinline__ float control_prologue(const RollParams &P, int k, int kg, int li,
                                                   bool active) {
-  float cc = 0.f;
+  const size_t row = (size_t)k * P.T;
   for (int t = li; t < P.T; t += G) {
     float u0, u1, c;
     control_at(P, k, kg, t, u0, u1, c);
-    cc += c;
     if (active) {
-      const size_t o = (size_t)k * P.T + t;
-      reinterpret_cast<float2 *>(P.u_out)[o] = make_float2(u0, u1);
+      reinterpret_cast<float2 *>(P.u_out)[row + t] = make_float2(u0, u1);
       float sd, cd;
       sincosf(u0, &sd, &cd);
-      P.ctl[o] = make_float4(u0, cd, sd, P.V.drive * u1);
+      P.ctl[row + t] = make_float4(u0, cd, sd, P.V.drive * u1);
+      P.ccost[row + t] = c;
     }
   }
   __syncwarp();
-  return group_sum<G>(cc);
+  // the reference adds the whole control cost before the stage costs
+  // (controllers.py:272-273); summing it in t order keeps every kernel
+  // (bss / smppi / mppi) bit-identical when the belief is degenerate
+  float cc = 0.f;
+  for (int t = 0; t < P.T; ++t) cc += P.ccost[row + t];
+  return cc;
 }
 
 // One particle-step: re-project (or load the persistent particle), Euler
@@ -262,7 +267,7 @@ __device__ __forceinline__ void particle_step(const RollParams &P, int t, int k,
 #pragma unroll
     for (int j = 0; j < 7; ++j) z[j] = zp[j];
   } else {
-    belief_normals(P.kb0, P.kb1, (uint32_t)t, (uint32_t)kg, (uint32_t)m, z);
+    belief_normals(P.kb, (uint32_t)t, (uint32_t)kg, (uint32_t)m, z);
   }
   if (PERSIST && t > 0) {
 #pragma unroll
@@ -412,24 +417,22 @@ __global__ void __launch_bounds__(kBlockThreads) bss_rollout_kernel(const RollPa
 // one lane per k, state carried in registers.
 template <bool SHIELD>
 __global__ void __launch_bounds__(kBlockThreads) det_rollout_kernel(const RollParams P) {
-  const int k = blockIdx.x * kBlockThreads + threadIdx.x;
-  if (k >= P.k_count) return;
-  const int kg = P.k_begin + k;
+  const int kraw = blockIdx.x * kBlockThreads + threadIdx.x;
+  if (kraw >= P.k_count) return;
+  const int k = kraw, kg = P.k_begin + k;
+  float total = control_prologue<1>(P, k, kg, 0, true);
   float x[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) x[i] = P.x0[i];
   float h_cur = SHIELD ? dcbf(x[6], 0.f, P) : 0.f;
   float h_prev = h_cur;
-  float total = 0.f;
   bool dead = false;
+  const float4 *ctl_row = P.ctl + (size_t)k * P.T;
   for (int t = 0; t < P.T; ++t) {
     total += stage_cost(x, P);
     if (SHIELD && t > 0) total += shield_penalty(h_cur, h_prev, P);
-    float u0, u1, cc;
-    control_at(P, k, kg, t, u0, u1, cc);
-    total += cc;
-    reinterpret_cast<float2 *>(P.u_out)[(size_t)k * P.T + t] = make_float2(u0, u1);
-    const bool ok = vehicle_step(x, make_ctl(u0, u1, P.V), P.V, P.tr);
+    const float4 cv = ctl_row[t];
+    const bool ok = vehicle_step(x, CtlDev{cv.x, cv.y, cv.z, cv.w}, P.V, P.tr);
     dead |= !ok;
     if (SHIELD) {
       h_prev = h_cur;
