@@ -115,7 +115,7 @@ int bssmppi_set_stream(bssmppi_ctx *ctx, void *cuda_stream);
  *   x0[8], cov0[16] (nullable => zero), plan[T*2] nominal.
  *   Noise: eps (K*T*2 post-factor perturbations) and z (T*K*M*7 standard
  *   normals, float) given => oracle-noise mode, consumed exactly like the
- *   reference; both NULL => device Philox4x32-10 keyed by key_ctrl / key_belief.
+ *   reference; both NULL => device Philox4x32 keyed by key_ctrl / key_belief.
  *   Output vplus[T*2] (the optimised sequence before the warm-start shift). */
 int bssmppi_control_step(bssmppi_ctx *ctx, const double *x0, const double *cov0,
                          const double *plan, const uint32_t key_ctrl[2],
@@ -176,9 +176,11 @@ int bssmppi_sample_controls(int32_t n, int32_t T, const double *z, const double 
 int bssmppi_step_array(bssmppi_ctx *ctx, int32_t n, const double *x, const double *u,
                        const double *w, double *x_out, uint8_t *ok);
 
-/* Test hooks for the device generator: Philox4x32-10 block function and the
+/* Test hooks for the device generator: the Philox4x32 block function
+ * (rounds = 10, the control stream, or 7, the belief stream) and the
  * per-particle-step normals the rollout consumes in Philox mode. */
-int bssmppi_philox4x32(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
+int bssmppi_philox4x32(const uint32_t ctr[4], const uint32_t key[2], int32_t rounds,
+                       uint32_t out[4]);
 int bssmppi_belief_normals(const uint32_t key[2], int32_t t, int32_t k, int32_t m_count,
                            float *out /* m_count*7 */);
 

@@ -16,7 +16,7 @@
  *   rollout_one()   _rollout bss/mppi/smppi controllers.py:261-341
  *   orc_update()    mppi_weights/mppi_update controllers.py:180-194
  * Noise: either the reference's captured arrays (eps (K,T,2), z (T,K,M,7))
- * or the device's Philox4x32-10 counters (same keys/counters as csrc/), so
+ * or the device's Philox4x32 counters (same keys/counters as csrc/), so
  * the timed CPU arm does the same work as the GPU arm.
  * Parallel over rollouts k with OpenMP (the reference parallelises only
  * across processes, sim.py:321-322; one k is independent of all others).
@@ -154,9 +154,9 @@ static void moments(const double *x, int n, double *buf, double *mean, double *c
     }
 }
 
-/* ---- Philox4x32-10 + Box-Muller: same counters as csrc/philox.cuh ---- */
-static void philox(uint32_t c[4], uint32_t k0, uint32_t k1) {
-  for (int i = 0; i < 10; ++i) {
+/* ---- Philox4x32 (7 rounds belief, 10 control) + Box-Muller: same counters as csrc/philox.cuh ---- */
+static void philox_r(uint32_t c[4], uint32_t k0, uint32_t k1, int rounds) {
+  for (int i = 0; i < rounds; ++i) {
     uint64_t p0 = (uint64_t)0xD2511F53u * c[0], p1 = (uint64_t)0xCD9E8D57u * c[2];
     uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0, hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
     uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
@@ -164,6 +164,9 @@ static void philox(uint32_t c[4], uint32_t k0, uint32_t k1) {
     k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
   }
 }
+
+/* rounds: 7 for the belief stream, 10 for the control stream (csrc/philox.cuh) */
+static void philox(uint32_t c[4], uint32_t k0, uint32_t k1) { philox_r(c, k0, k1, 10); }
 
 static void bm(uint32_t a, uint32_t b, double *z0, double *z1) {
   union { uint32_t u; float f; } x, y;
@@ -178,8 +181,8 @@ static void bm(uint32_t a, uint32_t b, double *z0, double *z1) {
 static void belief_normals(uint32_t k0, uint32_t k1, uint32_t t, uint32_t kg, uint32_t m, double z[7]) {
   uint32_t a[4] = {t, m, kg, 0u}, b[4] = {t, m, kg, 1u};
   double spare;
-  philox(a, k0, k1);
-  philox(b, k0, k1);
+  philox_r(a, k0, k1, 7);
+  philox_r(b, k0, k1, 7);
   bm(a[0], a[1], &z[0], &z[1]);
   bm(a[2], a[3], &z[2], &z[3]);
   bm(b[0], b[1], &z[4], &z[5]);
@@ -192,9 +195,9 @@ static void control_normals(uint32_t k0, uint32_t k1, uint32_t t, uint32_t kg, d
   bm(a[0], a[1], z0, z1);
 }
 
-int orc_philox4x32(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+int orc_philox4x32(const uint32_t ctr[4], const uint32_t key[2], int rounds, uint32_t out[4]) {
   uint32_t c[4] = {ctr[0], ctr[1], ctr[2], ctr[3]};
-  philox(c, key[0], key[1]);
+  philox_r(c, key[0], key[1], rounds);
   memcpy(out, c, sizeof(c));
   return 0;
 }

@@ -32,7 +32,7 @@ def load():
         lib.orc_update.argtypes = [C.c_int, C.c_int, _dp, _dp, C.c_double, _dp, _dp, _dp]
         lib.orc_control_step.argtypes = [C.POINTER(Problem), _dp, _dp, _dp, _u32p, _u32p, _dp, _dp,
                                          _dp, C.c_int]
-        lib.orc_philox4x32.argtypes = [_u32p, _u32p, _u32p]
+        lib.orc_philox4x32.argtypes = [_u32p, _u32p, C.c_int, _u32p]
         lib.orc_max_threads.restype = C.c_int
         _lib = lib
     return _lib
@@ -91,9 +91,9 @@ def control_step(problem, x0, cov0, plan, key_ctrl, key_belief, threads=0):
     return out, costs
 
 
-def philox(ctr, key):
+def philox(ctr, key, rounds=10):
     out = (C.c_uint32 * 4)()
-    load().orc_philox4x32((C.c_uint32 * 4)(*ctr), (C.c_uint32 * 2)(*key), out)
+    load().orc_philox4x32((C.c_uint32 * 4)(*ctr), (C.c_uint32 * 2)(*key), int(rounds), out)
     return list(out)
 
 

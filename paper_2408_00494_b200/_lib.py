@@ -84,7 +84,7 @@ SIGNATURES = {
     "bssmppi_sample_controls": (C.c_int, [C.c_int32, C.c_int32, _dp, _dp, _dp, _dp, _dp, _dp,
                                           _dp]),
     "bssmppi_step_array": (C.c_int, [_ctx, C.c_int32, _dp, _dp, _dp, _dp, _u8p]),
-    "bssmppi_philox4x32": (C.c_int, [_u32p, _u32p, _u32p]),
+    "bssmppi_philox4x32": (C.c_int, [_u32p, _u32p, C.c_int32, _u32p]),
     "bssmppi_belief_normals": (C.c_int, [_u32p, C.c_int32, C.c_int32, C.c_int32, _fp]),
     "bssmppi_ffma_peak": (C.c_int, [C.c_int32, _dp]),
 }

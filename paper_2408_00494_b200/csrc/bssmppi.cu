@@ -616,8 +616,9 @@ __global__ void __launch_bounds__(256) ffma_peak_kernel(float *out, int iters, f
   if (s == 12345.678f) out[0] = s;
 }
 
-__global__ void philox_kernel(Philox4 c, uint32_t k0, uint32_t k1, uint32_t *out) {
-  const Philox4 r = philox4x32_10(c, k0, k1);
+__global__ void philox_kernel(Philox4 c, uint32_t k0, uint32_t k1, int rounds, uint32_t *out) {
+  const PhiloxKeys rk = philox_schedule(k0, k1);
+  const Philox4 r = rounds == 7 ? philox4x32<7>(c, rk) : philox4x32<10>(c, rk);
   out[0] = r.x; out[1] = r.y; out[2] = r.z; out[3] = r.w;
 }
 
@@ -685,12 +686,13 @@ int bssmppi_step_array(bssmppi_ctx *c, int32_t n, const double *x, const double 
   return BSSMPPI_OK;
 }
 
-int bssmppi_philox4x32(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+int bssmppi_philox4x32(const uint32_t ctr[4], const uint32_t key[2], int32_t rounds, uint32_t out[4]) {
   if (!ctr || !key || !out) return fail(BSSMPPI_ERR_INVALID, "NULL argument");
+  if (rounds != 7 && rounds != 10) return fail(BSSMPPI_ERR_INVALID, "rounds must be 7 or 10");
   uint32_t *d = nullptr;
   int rc = dev_alloc(&d, 4);
   if (rc) return rc;
-  philox_kernel<<<1, 1>>>(Philox4{ctr[0], ctr[1], ctr[2], ctr[3]}, key[0], key[1], d);
+  philox_kernel<<<1, 1>>>(Philox4{ctr[0], ctr[1], ctr[2], ctr[3]}, key[0], key[1], rounds, d);
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaMemcpy(out, d, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost);
   cudaFree(d);

@@ -28,19 +28,6 @@ __host__ __device__ __forceinline__ void mulhilo32(uint32_t a, uint32_t b, uint3
 #endif
 }
 
-__host__ __device__ __forceinline__ Philox4 philox4x32_10(Philox4 c, uint32_t k0, uint32_t k1) {
-#pragma unroll
-  for (int i = 0; i < 10; ++i) {
-    uint32_t hi0, lo0, hi1, lo1;
-    mulhilo32(0xD2511F53u, c.x, hi0, lo0);
-    mulhilo32(0xCD9E8D57u, c.z, hi1, lo1);
-    c = Philox4{hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0};
-    k0 += 0x9E3779B9u;
-    k1 += 0xBB67AE85u;
-  }
-  return c;
-}
-
 // Round-key schedule k_i = k + i * (W0, W1), i = 0..9, precomputed on the
 // host once per iteration so the rounds read their keys as kernel-constant
 // operands instead of re-deriving them per call.
@@ -57,9 +44,19 @@ __host__ __device__ __forceinline__ PhiloxKeys philox_schedule(uint32_t k0, uint
   return r;
 }
 
-__host__ __device__ __forceinline__ Philox4 philox4x32_10(Philox4 c, const PhiloxKeys &rk) {
+// Rounds of the hot belief-noise generator: Philox4x32 with 7 rounds passes
+// TestU01 BigCrush (Salmon et al., SC'11, Table 2); 10 is Random123's
+// default safety margin and is kept for the (tiny) control-noise stream.
+#ifndef BSS_BELIEF_ROUNDS
+#define BSS_BELIEF_ROUNDS 7
+#endif
+constexpr int kBeliefRounds = BSS_BELIEF_ROUNDS;
+constexpr int kControlRounds = 10;
+
+template <int R>
+__host__ __device__ __forceinline__ Philox4 philox4x32(Philox4 c, const PhiloxKeys &rk) {
 #pragma unroll
-  for (int i = 0; i < 10; ++i) {
+  for (int i = 0; i < R; ++i) {
     uint32_t hi0, lo0, hi1, lo1;
     mulhilo32(0xD2511F53u, c.x, hi0, lo0);
     mulhilo32(0xCD9E8D57u, c.z, hi1, lo1);
@@ -95,13 +92,13 @@ __device__ __forceinline__ void box_muller1(uint32_t a, uint32_t b, float &z0) {
   z0 = r * __cosf(6.28318530718f * u2);
 }
 
-// The 7 standard normals of particle-step (t, k, m): [0:4] re-projection
+// The 7 standard normals of particle-step (t, k, m) (Philox4x32-7 counters): [0:4] re-projection
 // on the tracked subset, [4:7] process noise -- the column layout of the
 // reference's z_all block (controllers.py:285-287, belief.py:328-333).
 __device__ __forceinline__ void belief_normals(const PhiloxKeys &rk, uint32_t t, uint32_t kg,
                                                uint32_t m, float z[7]) {
-  const Philox4 a = philox4x32_10(Philox4{t, m, kg, 0u}, rk);
-  const Philox4 b = philox4x32_10(Philox4{t, m, kg, 1u}, rk);
+  const Philox4 a = philox4x32<kBeliefRounds>(Philox4{t, m, kg, 0u}, rk);
+  const Philox4 b = philox4x32<kBeliefRounds>(Philox4{t, m, kg, 1u}, rk);
   box_muller(a.x, a.y, z[0], z[1]);
   box_muller(a.z, a.w, z[2], z[3]);
   box_muller(b.x, b.y, z[4], z[5]);
@@ -111,7 +108,7 @@ __device__ __forceinline__ void belief_normals(const PhiloxKeys &rk, uint32_t t,
 // The 2 standard normals of control sample (k, t) (controllers.py:175).
 __device__ __forceinline__ void control_normals(const PhiloxKeys &rk, uint32_t t, uint32_t kg,
                                                 float &z0, float &z1) {
-  const Philox4 a = philox4x32_10(Philox4{t, kg, 0x5eedc0deu, 0u}, rk);
+  const Philox4 a = philox4x32<kControlRounds>(Philox4{t, kg, 0x5eedc0deu, 0u}, rk);
   box_muller(a.x, a.y, z0, z1);
 }
 #endif

@@ -215,6 +215,11 @@ __device__ __forceinline__ void group_allreduce18(float a[18], int li, float *sl
 
 constexpr int kSlotFloats = 20;   // 18 sums, 16-byte aligned slot
 constexpr int kBlockThreads = 128;
+// Register budget: 5 resident 128-thread blocks per SM (<= 102 registers,
+// 20 warps/SM) measured fastest at C3 (96 vs 113 registers: -2%).
+#ifndef BSS_MIN_BLOCKS
+#define BSS_MIN_BLOCKS 5
+#endif
 
 // Group-wide sum over G lanes (xor butterfly; every lane gets the total).
 template <int G>
@@ -312,7 +317,7 @@ __device__ __forceinline__ void accumulate(float acc[18], const float x[8], cons
 // shared memory instead of re-projecting (controllers.py:288-305);
 // ZARR: read the reference's normals instead of Philox.
 template <int G, bool PERSIST, bool ZARR>
-__global__ void __launch_bounds__(kBlockThreads) bss_rollout_kernel(const RollParams P) {
+__global__ void __launch_bounds__(kBlockThreads, BSS_MIN_BLOCKS) bss_rollout_kernel(const RollParams P) {
   extern __shared__ float4 smem4[];
   float *smem = reinterpret_cast<float *>(smem4);
   constexpr int GPW = 32 / G;

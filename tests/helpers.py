@@ -66,7 +66,7 @@ class Inputs:
         return costs, vplus
 
 
-def moments_rel_err(mean_a, cov_a, mean_b, cov_b):
+def moments_rel_err(mean_a, cov_a, mean_b, cov_b, floor=None):
     """SURVEY.md 8c moment metric: |dmu_i| / max(|mu_i|, sigma_i) over the
     tracked components (sigma from b) and |dSigma_ab| / sqrt(S_aa S_bb)."""
     if mean_a.size == 0:
@@ -75,6 +75,8 @@ def moments_rel_err(mean_a, cov_a, mean_b, cov_b):
     sig = np.sqrt(np.clip(np.diagonal(cov_b, axis1=-2, axis2=-1), 0, None))
     scale_m = np.abs(mean_b).copy()
     scale_m[..., sub] = np.maximum(scale_m[..., sub], sig)
+    if floor is not None:
+        scale_m = np.maximum(scale_m, floor)
     with np.errstate(divide="ignore", invalid="ignore"):
         em = np.abs(mean_a - mean_b) / scale_m
         em = np.where(scale_m == 0, np.where(mean_a == mean_b, 0.0, np.inf), em)

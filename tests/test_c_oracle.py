@@ -56,6 +56,12 @@ def test_philox_known_answers():
                                                         0x24126EA1]
 
 
+def test_philox_round_counts_differ():
+    a = c_oracle.philox([1, 2, 3, 4], [5, 6], rounds=7)
+    b = c_oracle.philox([1, 2, 3, 4], [5, 6], rounds=10)
+    assert a != b
+
+
 def test_philox_mode_thread_invariant():
     """Counter-based noise: the CPU arm's result does not depend on threads."""
     inp = Inputs("c1_s0")

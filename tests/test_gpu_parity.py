@@ -90,7 +90,13 @@ def test_belief_moments(name):
     # weightless; its moments after leaving the curvilinear frame are
     # frame-singular in both implementations)
     alive = np.broadcast_to(np.isfinite(gold["costs"][ks])[None, :], mean.shape[:2])
-    em, ec = moments_rel_err(mean[alive], cov[alive], gold["means"][alive], gold["covs"][alive])
+    # A degenerate belief (zero spread: sigma = 0) makes |dmu| / max(|mu|, sigma)
+    # ill-posed for components that pass near zero; floor the scale at 1e-2 of
+    # the component's own magnitude along the horizon.  (Exactness of the
+    # collapse itself is tested on the device: test_gpu_semantics.py.)
+    floor = 1e-2 * np.abs(gold["means"]).max(axis=0, keepdims=True)
+    em, ec = moments_rel_err(mean[alive], cov[alive], gold["means"][alive], gold["covs"][alive],
+                             floor=np.broadcast_to(floor, mean.shape)[alive])
     zero = gold["covs"][alive] == 0.0
     print(f"{name}: moments mean {em:.2e} cov {ec:.2e}")
     # With M < 16 particles the 4x4 sample covariance is nearly singular

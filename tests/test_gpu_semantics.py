@@ -48,8 +48,15 @@ def test_philox_device_known_answers():
                            [0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD]),
                           ([0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344], [0xA4093822, 0x299F31D0],
                            [0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1])]:
-        _lib.check(lib.bssmppi_philox4x32((_lib.C.c_uint32 * 4)(*ctr), (_lib.C.c_uint32 * 2)(*key), out))
+        _lib.check(lib.bssmppi_philox4x32((_lib.C.c_uint32 * 4)(*ctr), (_lib.C.c_uint32 * 2)(*key), 10, out))
         assert list(out) == exp
+    # the 7-round belief generator agrees with the C port bit for bit
+    rng = np.random.default_rng(1)
+    for _ in range(16):
+        ctr = [int(v) for v in rng.integers(0, 2 ** 32, 4)]
+        key = [int(v) for v in rng.integers(0, 2 ** 32, 2)]
+        _lib.check(lib.bssmppi_philox4x32((_lib.C.c_uint32 * 4)(*ctr), (_lib.C.c_uint32 * 2)(*key), 7, out))
+        assert list(out) == c_oracle.philox(ctr, key, rounds=7)
 
 
 def test_belief_normals_statistics():
@@ -64,6 +71,15 @@ def test_belief_normals_statistics():
     assert np.all(np.abs(c[np.triu_indices(7, 1)]) < 5 * se)
     # tails: P(|z| > 3) = 0.0027
     assert abs(np.mean(np.abs(z) > 3.0) - 0.0027) < 0.0006
+    # adjacent counters (m, m+1) are uncorrelated, and uniform bins are flat
+    a, b = z[:-1].astype(np.float64), z[1:].astype(np.float64)
+    lag = np.mean(a * b, 0)
+    assert np.all(np.abs(lag) < 5 * se)
+    from scipy.stats import chi2, norm
+    u = norm.cdf(z[:, 0].astype(np.float64))
+    hist = np.bincount(np.minimum((u * 64).astype(int), 63), minlength=64)
+    stat = ((hist - n / 64) ** 2 / (n / 64)).sum()
+    assert stat < chi2.ppf(0.9999, 63)
     z2 = np.empty_like(z)
     _lib.check(lib.bssmppi_belief_normals(_lib.key_arr((12345, 678)), 3, 77, n, _lib.fptr(z2)))
     assert np.array_equal(z, z2)
