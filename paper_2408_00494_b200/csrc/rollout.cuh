@@ -264,7 +264,8 @@ __device__ __forceinline__ float control_prologue(const RollParams &P, int k, in
 template <bool PERSIST, bool ZARR>
 __device__ __forceinline__ void particle_step(const RollParams &P, int t, int k, int kg, int m,
                                               const float mean[8], const float L[10],
-                                              const CtlDev &ctl, float *cloud, float x[8]) {
+                                              const CtlDev &ctl, const StepShared &sh, float *cloud,
+                                              float x[8]) {
   const int M = P.M;
   float z[7];
   if (ZARR) {
@@ -286,7 +287,10 @@ __device__ __forceinline__ void particle_step(const RollParams &P, int t, int k,
     x[5] += L[3] * z[0] + L[4] * z[1] + L[5] * z[2];
     x[6] += L[6] * z[0] + L[7] * z[1] + L[8] * z[2] + L[9] * z[3];
   }
-  vehicle_step(x, ctl, P.V, P.tr);       // per-particle ok is discarded (belief.py:370)
+  // per-particle ok is discarded (belief.py:370); a re-projected particle
+  // shares (vx, omega_f, omega_r, s) with the mean, hence the shared terms
+  if (PERSIST && t > 0) vehicle_step(x, ctl, P.V, P.tr);
+  else step_particle(x, sh, ctl, P.V, P.tr);
   if (P.noise_on) {                      // added after integration (dynamics.py:571-572)
     x[0] += P.F[0] * z[4] + P.F[1] * z[5] + P.F[2] * z[6];
     x[1] += P.F[3] * z[4] + P.F[4] * z[5] + P.F[5] * z[6];
@@ -356,6 +360,8 @@ __global__ void __launch_bounds__(kBlockThreads, BSS_MIN_BLOCKS) bss_rollout_ker
     if (t > 0) total += shield_penalty(h_cur, h_prev, P);
     const float4 cv = ctl_row[t];
     const CtlDev ctl{cv.x, cv.y, cv.z, cv.w};
+    StepShared sh;
+    if (!(PERSIST && t > 0)) sh = step_shared(mean, ctl, P.V, P.tr);
 
     // Particle 0 of the group doubles as the shift of the one-pass moments:
     // it sits O(sigma) from the mean, and a zero-spread cloud gives d == 0.
@@ -363,12 +369,12 @@ __global__ void __launch_bounds__(kBlockThreads, BSS_MIN_BLOCKS) bss_rollout_ker
 #pragma unroll
     for (int i = 0; i < 18; ++i) acc[i] = 0.f;
     float x[8], c[8];
-    if (has0) particle_step<PERSIST, ZARR>(P, t, k, kg, li, mean, L, ctl, cloud, x);
+    if (has0) particle_step<PERSIST, ZARR>(P, t, k, kg, li, mean, L, ctl, sh, cloud, x);
 #pragma unroll
     for (int i = 0; i < 8; ++i) c[i] = __shfl_sync(0xffffffffu, x[i], 0, G);
     if (has0) accumulate(acc, x, c);
     for (int m = li + G; m < M; m += G) {
-      particle_step<PERSIST, ZARR>(P, t, k, kg, m, mean, L, ctl, cloud, x);
+      particle_step<PERSIST, ZARR>(P, t, k, kg, m, mean, L, ctl, sh, cloud, x);
       accumulate(acc, x, c);
     }
     group_allreduce18<G>(acc, li, slots + (t & 1) * kSlotFloats);

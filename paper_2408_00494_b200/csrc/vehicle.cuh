@@ -83,67 +83,105 @@ __device__ __forceinline__ bool all_finite8(const float x[8]) {
   return fabsf(s) < __int_as_float(0x7f800000);
 }
 
-// One Euler step x <- x + dt f(x, u), wraps, non-finite -> 0.  Returns the
-// reference's per-particle ok (frame > 0 and finite).
-__device__ __forceinline__ bool vehicle_step(float x[8], const CtlDev &c, const VehDev &V,
-                                             const TrackDev &tr) {
-  const float vx = x[0], vy = x[1], r = x[2], wf = x[3], wr = x[4], ep = x[5], ey = x[6],
-              s = x[7];
+// The step split in two: everything that depends only on (vx, omega_f,
+// omega_r, s) and the control -- the longitudinal slips and tire forces,
+// the wheel accelerations and kappa(s) -- is `step_shared`; the rest, which
+// also depends on (vy, r, e_psi, e_y), is `step_particle`.  After Gaussian
+// re-projection (belief.py:264-272) all M particles of a rollout share
+// (vx, omega_f, omega_r, s) exactly, so the rollout kernel evaluates
+// step_shared once per (k, t) instead of once per particle.  vehicle_step()
+// is the composition, so every path computes bit-identical values.
+struct StepShared {
+  float vxe, rx, inv_den;     // low-speed-floored vx and its reciprocal
+  float fxf, fxr, cxf, cxr;   // longitudinal forces and |cos| friction-ellipse factors
+  float dvx_lon;              // (fxr) / m: rear longitudinal force term of dvx
+  float dwf, dwr;             // wheel accelerations (complete)
+  float kap;                  // kappa(s)
+};
+
+__device__ __forceinline__ StepShared step_shared(const float x[8], const CtlDev &c, const VehDev &V,
+                                                  const TrackDev &tr) {
+  const float vx = x[0], wf = x[3], wr = x[4], s = x[7];
+  StepShared h;
   // _tire_row: low-speed floor keeps the sign of vx.
-  const float vxe = (vx >= 0.f) ? fmaxf(vx, V.vfloor) : fminf(vx, -V.vfloor);
+  h.vxe = (vx >= 0.f) ? fmaxf(vx, V.vfloor) : fminf(vx, -V.vfloor);
 #ifdef BSS_EXACT_MATH
-  const float inv_den = 1.0f / fabsf(vxe);
-  const float af = c.delta - atan2f(vy + V.lf * r, vxe);
-  const float ar = -atan2f(vy - V.lr * r, vxe);
+  h.rx = 1.0f / h.vxe;
+  h.inv_den = 1.0f / fabsf(h.vxe);
 #else
-  const float rx = __frcp_rn(vxe);          // |vxe| >= v_floor > 0
-  const float inv_den = fabsf(rx);
-  const float af = c.delta - atan2_rcp(vy + V.lf * r, vxe, rx);
-  const float ar = -atan2_rcp(vy - V.lr * r, vxe, rx);
+  h.rx = __frcp_rn(h.vxe);           // |vxe| >= v_floor > 0
+  h.inv_den = fabsf(h.rx);
 #endif
-  const float sgf = (wf * V.R - vx) * inv_den;
-  const float sgr = (wr * V.R - vx) * inv_den;
-  const float tyf = V.Cyf * atanf(V.Byf * af), tyr = V.Cyr * atanf(V.Byr * ar);
+  const float sgf = (wf * V.R - vx) * h.inv_den;
+  const float sgr = (wr * V.R - vx) * h.inv_den;
   const float txf = V.Cxf * atanf(V.Bxf * sgf), txr = V.Cxr * atanf(V.Bxr * sgr);
-  float syf, syr, sxf, cxf, sxr, cxr;
-#ifndef BSS_EXACT_MATH
-#ifndef BSS_POLY_TIRE
-  // MUFU sin/cos (|error| ~3.6e-7 on |theta| <= 2.05): the parity harness
-  // shows the same moment/cost errors as the polynomial at ~7% less time
-  if (true) {
-    syf = __sinf(tyf); syr = __sinf(tyr);
-    __sincosf(txf, &sxf, &cxf);
-    __sincosf(txr, &sxr, &cxr);
-  } else
-#endif
+  float sxf, sxr;
+#if defined(BSS_EXACT_MATH)
+  sincosf(txf, &sxf, &h.cxf);
+  sincosf(txr, &sxr, &h.cxr);
+#elif defined(BSS_POLY_TIRE)
   if (V.mf_poly) {
-    syf = sin_mf(tyf); syr = sin_mf(tyr);
-    sxf = sin_mf(txf); cxf = cos_mf(txf);
-    sxr = sin_mf(txr); cxr = cos_mf(txr);
-  } else
-#endif
-  {
-    syf = sinf(tyf); syr = sinf(tyr);
-    sincosf(txf, &sxf, &cxf);
-    sincosf(txr, &sxr, &cxr);
+    sxf = sin_mf(txf); h.cxf = cos_mf(txf);
+    sxr = sin_mf(txr); h.cxr = cos_mf(txr);
+  } else {
+    sincosf(txf, &sxf, &h.cxf);
+    sincosf(txr, &sxr, &h.cxr);
   }
-  const float fxf = V.Dxf * sxf, fxr = V.Dxr * sxr;
-  const float fyf = V.Dyf * syf * fabsf(cxf), fyr = V.Dyr * syr * fabsf(cxr);
-  // _derivs_row
-  const float fxb = fxf * c.cd - fyf * c.sd;
-  const float fyb = fxf * c.sd + fyf * c.cd;
-  const float dvx = (fxb + fxr) * V.inv_m + vy * r;
-  const float dvy = (fyb + fyr) * V.inv_m - vx * r;
-  const float dr = (V.lf * fyb - V.lr * fyr) * V.inv_iz;
+#else
+  // MUFU sin/cos (|error| ~3.6e-7 on |theta| <= 2.05): same parity as the
+  // polynomial in the harness at less cost
+  __sincosf(txf, &sxf, &h.cxf);
+  __sincosf(txr, &sxr, &h.cxr);
+#endif
+  h.cxf = fabsf(h.cxf);
+  h.cxr = fabsf(h.cxr);
+  h.fxf = V.Dxf * sxf;
+  h.fxr = V.Dxr * sxr;
+  h.dvx_lon = h.fxr;
+  // _derivs_row wheel torque balance; rolling resistance opposes the spin
 #ifdef BSS_EXACT_MATH
   const float spf = tanhf(wf * V.spin_scale), spr = tanhf(wr * V.spin_scale);
 #else
   const float spf = tanh_sat(wf * V.spin_scale), spr = tanh_sat(wr * V.spin_scale);
 #endif
-  const float dwf = (-V.R * fxf - V.rrf * spf) * V.inv_jw;
-  const float dwr = (c.drive_u1 - V.R * fxr - V.rrr * spr) * V.inv_jw;
-  const float kap = curvature(tr, s);
-  float frame = 1.f - kap * ey;
+  h.dwf = (-V.R * h.fxf - V.rrf * spf) * V.inv_jw;
+  h.dwr = (c.drive_u1 - V.R * h.fxr - V.rrr * spr) * V.inv_jw;
+  h.kap = curvature(tr, s);
+  return h;
+}
+
+// One Euler step x <- x + dt f(x, u), wraps, non-finite -> 0, given the
+// shared terms of x.  Returns the reference's per-particle ok (frame > 0
+// and finite).
+__device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, const CtlDev &c,
+                                              const VehDev &V, const TrackDev &tr) {
+  const float vx = x[0], vy = x[1], r = x[2], wf = x[3], wr = x[4], ep = x[5], ey = x[6],
+              s = x[7];
+#ifdef BSS_EXACT_MATH
+  const float af = c.delta - atan2f(vy + V.lf * r, h.vxe);
+  const float ar = -atan2f(vy - V.lr * r, h.vxe);
+#else
+  const float af = c.delta - atan2_rcp(vy + V.lf * r, h.vxe, h.rx);
+  const float ar = -atan2_rcp(vy - V.lr * r, h.vxe, h.rx);
+#endif
+  const float tyf = V.Cyf * atanf(V.Byf * af), tyr = V.Cyr * atanf(V.Byr * ar);
+  float syf, syr;
+#if defined(BSS_EXACT_MATH)
+  syf = sinf(tyf); syr = sinf(tyr);
+#elif defined(BSS_POLY_TIRE)
+  if (V.mf_poly) { syf = sin_mf(tyf); syr = sin_mf(tyr); }
+  else { syf = sinf(tyf); syr = sinf(tyr); }
+#else
+  syf = __sinf(tyf); syr = __sinf(tyr);
+#endif
+  const float fyf = V.Dyf * syf * h.cxf, fyr = V.Dyr * syr * h.cxr;
+  // _derivs_row
+  const float fxb = h.fxf * c.cd - fyf * c.sd;
+  const float fyb = h.fxf * c.sd + fyf * c.cd;
+  const float dvx = (fxb + h.dvx_lon) * V.inv_m + vy * r;
+  const float dvy = (fyb + fyr) * V.inv_m - vx * r;
+  const float dr = (V.lf * fyb - V.lr * fyr) * V.inv_iz;
+  float frame = 1.f - h.kap * ey;
   bool ok = frame > 0.f;
   if (frame < 1e-3f) frame = 1e-3f;
   float se, ce;
@@ -155,13 +193,13 @@ __device__ __forceinline__ bool vehicle_step(float x[8], const CtlDev &c, const 
   const float ds = __fdividef(vx * ce - vy * se, frame);   // frame in [1e-3, 1 + kappa w]
 #endif
   const float dey = vx * se + vy * ce;
-  const float dep = r - kap * ds;
+  const float dep = r - h.kap * ds;
   // _step_kernel Euler branch + wraps
   x[0] = vx + V.dt * dvx;
   x[1] = vy + V.dt * dvy;
   x[2] = r + V.dt * dr;
-  x[3] = wf + V.dt * dwf;
-  x[4] = wr + V.dt * dwr;
+  x[3] = wf + V.dt * h.dwf;
+  x[4] = wr + V.dt * h.dwr;
   x[5] = wrap_pi(ep + V.dt * dep);
   x[6] = ey + V.dt * dey;
   const float s1 = s + V.dt * ds;
@@ -176,6 +214,12 @@ __device__ __forceinline__ bool vehicle_step(float x[8], const CtlDev &c, const 
     ok = ok && fin;
   }
   return ok;
+}
+
+__device__ __forceinline__ bool vehicle_step(float x[8], const CtlDev &c, const VehDev &V,
+                                             const TrackDev &tr) {
+  const StepShared h = step_shared(x, c, V, tr);
+  return step_particle(x, h, c, V, tr);
 }
 
 __device__ __forceinline__ CtlDev make_ctl(float delta, float throttle, const VehDev &V) {
