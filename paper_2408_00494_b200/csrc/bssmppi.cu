@@ -189,6 +189,9 @@ void fill_params(bssmppi_ctx *c, const bssmppi_problem *p) {
   bool any = false;
   for (int i = 0; i < 9; ++i) { r.F[i] = (float)p->noise_factor[i]; any |= p->noise_factor[i] != 0.0; }
   r.noise_on = any ? 1 : 0;
+  const double *F = p->noise_factor;
+  r.noise_diag = (any && F[1] == 0.0 && F[2] == 0.0 && F[3] == 0.0 && F[5] == 0.0 && F[6] == 0.0 &&
+                  F[7] == 0.0) ? 1 : 0;
   r.shield = p->kind == BSSMPPI_KIND_SMPPI ? 1 : 0;
   r.chol_rank = std::min(4, std::max(1, r.M - 1));
 }

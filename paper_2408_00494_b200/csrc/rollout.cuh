@@ -37,6 +37,7 @@ struct RollParams {
   int k_count, k_begin, T, M;
   int ctrl_mode;      // CtrlMode
   int noise_on;       // process noise nonzero (dynamics.py:571 skips the add otherwise)
+  int noise_diag;     // noise factor is diagonal: 3 multiplies instead of a 3x3 product
   int shield;         // det kinds: 1 = smppi
   float invM, invMm1;
   float q[8];
@@ -291,7 +292,11 @@ __device__ __forceinline__ void particle_step(const RollParams &P, int t, int k,
   // shares (vx, omega_f, omega_r, s) with the mean, hence the shared terms
   if (PERSIST && t > 0) vehicle_step(x, ctl, P.V, P.tr);
   else step_particle(x, sh, ctl, P.V, P.tr);
-  if (P.noise_on) {                      // added after integration (dynamics.py:571-572)
+  if (P.noise_diag) {                    // added after integration (dynamics.py:571-572)
+    x[0] = fmaf(P.F[0], z[4], x[0]);
+    x[1] = fmaf(P.F[4], z[5], x[1]);
+    x[2] = fmaf(P.F[8], z[6], x[2]);
+  } else if (P.noise_on) {
     x[0] += P.F[0] * z[4] + P.F[1] * z[5] + P.F[2] * z[6];
     x[1] += P.F[3] * z[4] + P.F[4] * z[5] + P.F[5] * z[6];
     x[2] += P.F[6] * z[4] + P.F[7] * z[5] + P.F[8] * z[6];

@@ -43,23 +43,31 @@ struct CtlDev {
 
 // Python/numba floor-mod (dynamics.py:486-489): result in [0, L], with
 // (-tiny) % L == L.  Exact for x in [-L, 2L) (Sterbenz), fmodf otherwise.
-__device__ __forceinline__ float floor_mod(float x, float L) {
-  if (x >= 0.f && x < L) return x;
-  if (x >= L && x < 2.f * L) return x - L;
-  if (x < 0.f && x >= -L) return x + L;
+__device__ __noinline__ float floor_mod_slow(float x, float L) {
   float r = fmodf(x, L);
   if (r < 0.f) r += L;
   return r;
+}
+
+__device__ __forceinline__ float floor_mod(float x, float L) {
+  // fast path covers x in [-L, 2L) exactly (Sterbenz / Python semantics)
+  const float r = (x >= L) ? x - L : ((x < 0.f) ? x + L : x);
+  if (__builtin_expect(x >= -L && x < 2.f * L, 1)) return r;
+  return floor_mod_slow(x, L);
 }
 
 // pi - ((pi - a) mod 2pi) (dynamics.py:486).  Inside (-pi, pi] this is the
 // identity (to 1e-16 in the FP64 reference); evaluating it literally in FP32
 // would quantise every heading error to ulp(pi) = 2.4e-7 rad, so the
 // formula is applied only when a wrap actually happens.
-__device__ __forceinline__ float wrap_pi(float a) {
+__device__ __noinline__ float wrap_pi_slow(float a) {
   const float PI = 3.14159265358979f, TWO_PI = 6.28318530717959f;
-  if (a > -PI && a <= PI) return a;
   return PI - floor_mod(PI - a, TWO_PI);
+}
+
+__device__ __forceinline__ float wrap_pi(float a) {
+  if (__builtin_expect(a > -3.14159265358979f && a <= 3.14159265358979f, 1)) return a;
+  return wrap_pi_slow(a);
 }
 
 __device__ __forceinline__ float curvature(const TrackDev &tr, float s) {
@@ -74,6 +82,16 @@ __device__ __forceinline__ float curvature(const TrackDev &tr, float s) {
     nd = __ldg(tr.node + lo + 1);
   }
   return fmaf(nd.z, sw - nd.x, nd.y);
+}
+
+// Non-finite components -> 0 (dynamics.py:493-496); returns "all finite".
+__device__ __noinline__ bool scrub_nonfinite(float *x) {
+  bool fin = true;
+  for (int i = 0; i < 8; ++i) {
+    fin &= isfinite(x[i]);
+    x[i] = isfinite(x[i]) ? x[i] : 0.f;
+  }
+  return fin;
 }
 
 // Fast screen: a sum of finite values is finite unless it overflows (then
@@ -204,15 +222,7 @@ __device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, c
   x[6] = ey + V.dt * dey;
   const float s1 = s + V.dt * ds;
   x[7] = tr.closed ? floor_mod(s1, tr.L) : fminf(fmaxf(s1, 0.f), tr.L);
-  if (!all_finite8(x)) {
-    bool fin = true;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      fin &= isfinite(x[i]);
-      x[i] = isfinite(x[i]) ? x[i] : 0.f;
-    }
-    ok = ok && fin;
-  }
+  if (__builtin_expect(!all_finite8(x), 0)) ok = scrub_nonfinite(x) && ok;
   return ok;
 }
 
