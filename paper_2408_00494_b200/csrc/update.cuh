@@ -103,8 +103,9 @@ update_partials_kernel(int n, int k_begin, int T2, const CT *costs, const UT *u,
   }
 }
 
-// Combine `nrec` records.  final == 0: write one record to rec_out.
-// final == 1: v+ = clip(N/Z) -> vplus (double), warm-start shifted plan
+// Combine `nrec` records (<= 1024), block-parallel and in a fixed order
+// (deterministic).  final == 0: write one record to rec_out.  final == 1:
+// v+ = clip(N/Z) -> vplus (double), warm-start shifted plan
 // (ControlPlan.shifted, controllers.py:154-156) -> plan_out (float, may be
 // null), head {beta, Z, Z2, n, argmin} -> head_out.
 __global__ void __launch_bounds__(kUpdThreads)
@@ -112,36 +113,64 @@ combine_kernel(int nrec, int T2, const double *rec, double lam, int final_, doub
                double lo0, double lo1, double hi0, double hi1, double *vplus, float *plan_out,
                double *head_out) {
   __shared__ double s_scale[1024];
+  __shared__ double s_a[kUpdThreads], s_b[kUpdThreads], s_c[kUpdThreads];
+  __shared__ long long s_i[kUpdThreads];
   __shared__ double s_head[kRecHead];
   const int tid = threadIdx.x;
   const int R = kRecHead + T2;
+  const double INF = __longlong_as_double(0x7ff0000000000000ll);
+  // 1. global minimum (ties -> smallest k) and finite count
+  double mn = INF, cnt = 0.0;
+  long long arg = -1;
+  for (int r = tid; r < nrec; r += kUpdThreads) {
+    const double *h = rec + (size_t)r * R;
+    if (h[3] > 0.0) {
+      cnt += h[3];
+      const long long a = (long long)h[4];
+      if (h[0] < mn || (h[0] == mn && (arg < 0 || a < arg))) { mn = h[0]; arg = a; }
+    }
+  }
+  s_a[tid] = mn; s_i[tid] = arg; s_c[tid] = cnt;
+  __syncthreads();
+  for (int s = kUpdThreads / 2; s > 0; s >>= 1) {
+    if (tid < s) {
+      const double a = s_a[tid], b = s_a[tid + s];
+      const long long ia = s_i[tid], ib = s_i[tid + s];
+      if (b < a || (b == a && ib >= 0 && (ia < 0 || ib < ia))) { s_a[tid] = b; s_i[tid] = ib; }
+      s_c[tid] += s_c[tid + s];
+    }
+    __syncthreads();
+  }
+  const double beta = s_a[0];
+  const long long argmin = s_i[0];
+  const double n = s_c[0];
+  __syncthreads();
+  // 2. rescale factors exp(-(beta_r - beta)/lambda); Z, Z2
+  double z = 0.0, z2 = 0.0;
+  for (int r = tid; r < nrec; r += kUpdThreads) {
+    const double *h = rec + (size_t)r * R;
+    const double sc = (h[3] > 0.0) ? exp(-(h[0] - beta) / lam) : 0.0;
+    s_scale[r] = sc;
+    z += sc * h[1];
+    z2 += sc * sc * h[2];
+  }
+  s_a[tid] = z; s_b[tid] = z2;
+  __syncthreads();
+  for (int s = kUpdThreads / 2; s > 0; s >>= 1) {
+    if (tid < s) { s_a[tid] += s_a[tid + s]; s_b[tid] += s_b[tid + s]; }
+    __syncthreads();
+  }
   if (tid == 0) {
-    double beta = __longlong_as_double(0x7ff0000000000000ll), arg = -1.0, n = 0.0;
-    for (int r = 0; r < nrec; ++r) {
-      const double *h = rec + (size_t)r * R;
-      if (h[3] > 0.0) {
-        n += h[3];
-        if (h[0] < beta || (h[0] == beta && (arg < 0.0 || h[4] < arg))) { beta = h[0]; arg = h[4]; }
-      }
-    }
-    double z = 0.0, z2 = 0.0;
-    for (int r = 0; r < nrec; ++r) {
-      const double *h = rec + (size_t)r * R;
-      double sc = 0.0;
-      if (h[3] > 0.0) sc = exp(-(h[0] - beta) / lam);
-      if (r < 1024) s_scale[r] = sc;
-      z += sc * h[1];
-      z2 += sc * sc * h[2];
-    }
-    s_head[0] = beta; s_head[1] = z; s_head[2] = z2; s_head[3] = n; s_head[4] = arg;
+    s_head[0] = beta; s_head[1] = s_a[0]; s_head[2] = s_b[0]; s_head[3] = n;
+    s_head[4] = (double)argmin;
   }
   __syncthreads();
+  // 3. N[col] = sum_r scale_r N_r[col] (records with n_r = 0 carry N_r = 0)
   for (int col = tid; col < T2; col += kUpdThreads) {
+    const double *src = rec + kRecHead + col;
     double a = 0.0;
-    for (int r = 0; r < nrec; ++r) {
-      const double sc = (r < 1024) ? s_scale[r] : 0.0;
-      if (sc != 0.0) a = fma(sc, rec[(size_t)r * R + kRecHead + col], a);
-    }
+#pragma unroll 8
+    for (int r = 0; r < nrec; ++r) a = fma(s_scale[r], src[(size_t)r * R], a);
     if (!final_) {
       rec_out[kRecHead + col] = a;
     } else {
@@ -156,7 +185,6 @@ combine_kernel(int nrec, int T2, const double *rec, double lam, int final_, doub
   }
   if (final_ && plan_out != nullptr) {
     __syncthreads();
-    __threadfence_block();
     for (int col = tid; col < T2; col += kUpdThreads) {
       const int src = (col + 2 < T2) ? col + 2 : col;   // drop first, repeat last
       plan_out[col] = (float)vplus[src];
