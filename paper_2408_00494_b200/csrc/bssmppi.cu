@@ -196,10 +196,16 @@ void fill_params(bssmppi_ctx *c, const bssmppi_problem *p) {
   r.chol_rank = std::min(4, std::max(1, r.M - 1));
 }
 
-int group_width(int M) {
-  if (M >= 32) return 32;
+// Lanes per rollout.  Start from one warp (or the power of two >= M), then
+// narrow the group while each lane would own < 4 particles and the GLOBAL
+// rollout count still fills the device (>= 2 waves of 20 warps x 148 SMs):
+// the per-(k, t) work (shared step terms, reduction, Cholesky, costs) is then
+// amortised over >= 4 particles.  Depends only on (M, K), never on the
+// shard, so every rank and G produces the same per-rollout arithmetic.
+int group_width(int M, int K) {
   int g = 2;
-  while (g < M) g <<= 1;
+  while (g < M && g < 32) g <<= 1;
+  while (g > 4 && M < 4 * g && (long long)K * g / 32 >= 2LL * 148 * 20) g >>= 1;
   return g;
 }
 
@@ -223,7 +229,7 @@ cudaError_t launch_bss_g(const RollParams &rp, bool persist, bool zarr, cudaStre
 int launch_rollout(bssmppi_ctx *c, const RollParams &rp, bool zarr) {
   cudaError_t e;
   if (c->kind == BSSMPPI_KIND_BSS) {
-    switch (group_width(rp.M)) {
+    switch (group_width(rp.M, c->K)) {
       case 2: e = launch_bss_g<2>(rp, c->persist, zarr, c->stream); break;
       case 4: e = launch_bss_g<4>(rp, c->persist, zarr, c->stream); break;
       case 8: e = launch_bss_g<8>(rp, c->persist, zarr, c->stream); break;
