@@ -151,3 +151,28 @@ def update_batch(j):
     costs[rng.choice(K, n_inf, replace=False)] = np.inf
     controls = rng.uniform(-0.6, 1.2, size=(K, T, 2))
     return costs, controls, lam
+
+
+# Closed-loop cases (reference sim.run_closed_loop, sim.py:232-309): the C2
+# setting (ellipse, dt 0.05, plant RK4 at 0.01) at parity-test sizes.
+CLOSED_LOOP = [
+    dict(name="cl_bss", K=256, M=32, T=20, steps=60, seed=3, run=0, noise_std=0.05,
+         init_speed=3.0, track="ellipse"),
+    dict(name="cl_bss_r1", K=256, M=32, T=20, steps=60, seed=3, run=1, noise_std=0.05,
+         init_speed=3.0, track="ellipse"),
+]
+
+
+def build_closed_loop(case, mods, sim_mod):
+    """ExperimentConfig for a closed-loop case in either module namespace
+    (mods: dynamics/controller types; sim_mod: the sim module)."""
+    from paper_2408_00494_b200.tracks import named_track
+
+    track = named_track(case["track"], build=mods.make_test_track)
+    cfg = mods.MppiConfig(kind="bss", samples=case["K"], horizon=case["T"], inner_samples=case["M"],
+                          sigma_eps=np.asarray(ELLIPSE_SIGMA_EPS))
+    noise = mods.NoiseModel(np.diag([case["noise_std"] ** 2] * 3))
+    kw = dict(controller=cfg, cost=mods.CostSpec(), vehicle=mods.VehicleParams(), track=track,
+              noise=noise, dt_control=0.05, dt_plant=0.01, master_seed=case["seed"],
+              max_steps=case["steps"], init_speed=case["init_speed"], collision_threshold=1.2)
+    return sim_mod.ExperimentConfig(**kw)

@@ -31,7 +31,8 @@ import belief_mppi.controllers as rc  # noqa: E402
 from belief_mppi import dynamics as rd  # noqa: E402
 from belief_mppi.streams import substream  # noqa: E402
 
-from cases import CASES, UPDATE_BATCHES, build, update_batch  # noqa: E402
+from cases import CASES, CLOSED_LOOP, UPDATE_BATCHES, build, build_closed_loop, update_batch  # noqa: E402
+from belief_mppi import sim as rsim  # noqa: E402
 
 REF = types.SimpleNamespace(
     VehicleParams=rd.VehicleParams, VehicleState=rd.VehicleState, NoiseModel=rd.NoiseModel,
@@ -121,6 +122,38 @@ def update_law_vectors():
     print("update_law: 4 batches")
 
 
+def closed_loop_vectors():
+    """Reference closed-loop trajectories (sim.run_closed_loop with
+    record_trajectory) for tests/test_gpu_closed_loop.py."""
+    for case in CLOSED_LOOP:
+        cfg = build_closed_loop(case, REF, rsim)
+        cfg.record_trajectory = True
+        rec = rsim.run_closed_loop(cfg, case["run"])
+        np.savez_compressed(HERE / f"{case['name']}.npz", meta=json.dumps(case),
+                            trajectory=rec.trajectory, crashed=np.array([rec.crashed]),
+                            steps=np.array([rec.steps]), collisions=np.array([rec.collisions]))
+        print(f"{case['name']}: steps={rec.steps} crashed={rec.crashed} collisions={rec.collisions}")
+
+
+def plant_vectors():
+    """Reference RK4 plant steps (step_array with the plant params) on random
+    states, for the host plant restatement (tests/test_sim_cpu.py)."""
+    from paper_2408_00494_b200.tracks import named_track
+    rng = np.random.default_rng(5)
+    track = named_track("ellipse", build=rd.make_test_track)
+    plant = rd.with_timestep(rd.VehicleParams(), 0.01, "rk4")
+    n = 256
+    x = np.zeros((n, 8))
+    x[:, 0] = rng.uniform(0.5, 7, n); x[:, 1] = rng.normal(0, 0.3, n); x[:, 2] = rng.normal(0, 0.5, n)
+    x[:, 3] = x[:, 0] / 0.095 * rng.uniform(0.8, 1.3, n); x[:, 4] = x[:, 0] / 0.095 * rng.uniform(0.8, 1.3, n)
+    x[:, 5] = rng.normal(0, 0.3, n); x[:, 6] = rng.uniform(-1.4, 1.4, n); x[:, 7] = rng.uniform(0, track.length, n)
+    u = np.stack([rng.uniform(-0.35, 0.35, n), rng.uniform(-1, 1, n)], 1)
+    w = rng.normal(0, 0.05, (n, 3))
+    out, ok = rd.step_array(x, u, w, plant, track)
+    np.savez_compressed(HERE / "plant_rk4.npz", x=x, u=u, w=w, out=out, ok=ok)
+    print("plant_rk4: 256 states")
+
+
 if __name__ == "__main__":
     os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
     names = set(sys.argv[1:])
@@ -129,3 +162,7 @@ if __name__ == "__main__":
             run_case(c)
     if not names or "update_law" in names:
         update_law_vectors()
+    if not names or "closed_loop" in names:
+        closed_loop_vectors()
+    if not names or "plant" in names:
+        plant_vectors()
