@@ -201,13 +201,18 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="C3", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="C3",
+                    help="one of %s, or C5:K:M for the BASELINE config-5 sweep (T=60)" % sorted(WORKLOADS))
     ap.add_argument("--e2e-steps", type=int, default=50)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-step-seconds", type=float, default=1.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
-    wl = WORKLOADS[args.workload]
+    if args.workload.startswith("C5:"):
+        _, k, m = args.workload.split(":")
+        wl = dict(K=int(k), M=int(m), T=60, dt=0.04, track="spline0", noise_std=0.05)
+    else:
+        wl = WORKLOADS[args.workload]
     if args.impl == "reference":
         return reference_arm(args, wl)
 
@@ -325,7 +330,7 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32 (FP64 weighted update)",
-        "data": "synthetic (seeded spline track, seeded x0, in-kernel Philox4x32-10 noise)",
+        "data": "synthetic (seeded spline track, seeded x0, in-kernel Philox4x32 noise)",
         "config": workload_config(args, wl),
         "e2e": {"value": KMT / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
                 "wall_ms_per_step": wall_e2e * 1e3,

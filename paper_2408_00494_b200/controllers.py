@@ -10,7 +10,8 @@ Numerics: all rollouts, belief moments, costs and the weighted update run
 in ``libbssmppi.so`` (csrc/).  Two noise sources:
 
 * ``noise_source="philox"`` (default, performance mode): control and belief
-  normals come from the in-kernel Philox4x32-10 generator keyed by the
+  normals come from the in-kernel Philox4x32 generator (7 rounds for the
+  belief stream, 10 for the control stream) keyed by the
   reference's (seed, *run_path, domain, iteration) identity;
 * ``noise_source="reference"`` (oracle-noise mode): the normals are drawn
   from the reference's own numpy substreams (controllers.py:384-393,

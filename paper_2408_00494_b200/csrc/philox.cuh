@@ -1,6 +1,6 @@
 // Counter-based normal generator for performance mode.
 //
-// Philox4x32-10 (Salmon et al., SC'11) keyed per (seed, run_path, domain,
+// Philox4x32 (Salmon et al., SC'11; 7 rounds belief, 10 control) keyed per (seed, run_path, domain,
 // iteration) -- the same identity as the reference's keyed numpy substreams
 // (streams.py:21-28) -- with counters built from (t, global k, m), so every
 // normal is a pure function of its coordinates: results do not depend on

@@ -5,7 +5,7 @@ mode of the controller draws its control perturbations and belief normals
 from it, exactly like the reference, and ships them to the device.
 
 ``device_key`` derives the 64-bit key of the *device* counter-based
-generator (Philox4x32-10, ``csrc/philox.cuh``) from the same
+generator (Philox4x32, ``csrc/philox.cuh``) from the same
 (root seed, *path) identity, so performance-mode streams are keyed by the
 same (seed, run_path, domain, iteration) tuple and stay independent of
 scheduling, sharding and worker count.
