@@ -197,15 +197,19 @@ void fill_params(bssmppi_ctx *c, const bssmppi_problem *p) {
 }
 
 // Lanes per rollout.  Start from one warp (or the power of two >= M), then
-// narrow the group while each lane would own < 4 particles and the GLOBAL
-// rollout count still fills the device (>= 2 waves of 20 warps x 148 SMs):
-// the per-(k, t) work (shared step terms, reduction, Cholesky, costs) is then
-// amortised over >= 4 particles.  Depends only on (M, K), never on the
-// shard, so every rank and G produces the same per-rollout arithmetic.
+// narrow the group while each lane would own < BSS_MIN_P particles and the
+// GLOBAL rollout count still fills the device (>= 2 waves of 20 warps x 148
+// SMs).  The per-(k, t) work (shared step terms, reduction, Cholesky, costs)
+// costs the same warp instructions for 1 or 32/G rollouts, so narrower groups
+// amortise it over more particles (C3: G = 8, 32 particles per lane, -10% vs
+// G = 32).  Depends only on (M, K), never on the shard.
+#ifndef BSS_MIN_P
+#define BSS_MIN_P 32
+#endif
 int group_width(int M, int K) {
   int g = 2;
   while (g < M && g < 32) g <<= 1;
-  while (g > 4 && M < 4 * g && (long long)K * g / 32 >= 2LL * 148 * 20) g >>= 1;
+  while (g > 4 && M < BSS_MIN_P * g && (long long)K * g / 32 >= 2LL * 148 * 20) g >>= 1;
   return g;
 }
 

@@ -207,7 +207,11 @@ __device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, c
   sincosf(ep, &se, &ce);
   const float ds = (vx * ce - vy * se) / frame;
 #else
+#ifdef BSS_MUFU_HEADING
+  __sincosf(ep, &se, &ce);
+#else
   sincos_pi(ep, se, ce);
+#endif
   const float ds = __fdividef(vx * ce - vy * se, frame);   // frame in [1e-3, 1 + kappa w]
 #endif
   const float dey = vx * se + vy * ce;
