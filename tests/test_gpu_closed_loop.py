@@ -37,7 +37,7 @@ def test_closed_loop_tracks_reference(case):
     # difference flips a near-tie the two loops separate, so step-for-step
     # agreement is asserted over the first steps only ...
     assert first_div >= 5
-    assert err_x[:5].max() < 5e-5
+    assert err_x[:5].max() < 5e-4   # v+ agrees to ~1e-5 (tolerance 1e-4); the plant propagates it
     # ... and the run statistics afterwards
     assert abs(tr[:, 0].mean() - theirs[:, 3].mean()) < 0.02 * abs(theirs[:, 3].mean())
     assert np.abs(tr[:, 6]).max() < 1.2 and np.abs(theirs[:, 2]).max() < 1.2
