@@ -184,6 +184,11 @@ int bssmppi_philox4x32(const uint32_t ctr[4], const uint32_t key[2], int32_t rou
 int bssmppi_belief_normals(const uint32_t key[2], int32_t t, int32_t k, int32_t m_count,
                            float *out /* m_count*7 */);
 
+/* Per-iteration device-noise key: Philox4x32-10 of (iteration, domain) under
+ * the controller's base key (host-side, no device work). */
+int bssmppi_iteration_key(const uint32_t base[2], uint32_t domain, uint64_t iteration,
+                          uint32_t out[2]);
+
 /* Measured FP32 FFMA throughput of the device (roofline denominator). */
 int bssmppi_ffma_peak(int32_t device, double *tflops);
 

@@ -195,6 +195,15 @@ static void control_normals(uint32_t k0, uint32_t k1, uint32_t t, uint32_t kg, d
   bm(a[0], a[1], z0, z1);
 }
 
+/* Per-iteration key (same definition as bssmppi_iteration_key). */
+int orc_iteration_key(const uint32_t base[2], uint32_t domain, uint64_t iteration, uint32_t out[2]) {
+  uint32_t c[4] = {(uint32_t)iteration, (uint32_t)(iteration >> 32), domain, 0x6b657973u};
+  philox_r(c, base[0], base[1], 10);
+  out[0] = c[0];
+  out[1] = c[1];
+  return 0;
+}
+
 int orc_philox4x32(const uint32_t ctr[4], const uint32_t key[2], int rounds, uint32_t out[4]) {
   uint32_t c[4] = {ctr[0], ctr[1], ctr[2], ctr[3]};
   philox_r(c, key[0], key[1], rounds);

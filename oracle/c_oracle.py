@@ -34,6 +34,7 @@ def load():
                                          _dp, C.c_int]
         lib.orc_philox4x32.argtypes = [_u32p, _u32p, C.c_int, _u32p]
         lib.orc_max_threads.restype = C.c_int
+        lib.orc_iteration_key.argtypes = [_u32p, C.c_uint32, C.c_uint64, _u32p]
         _lib = lib
     return _lib
 
@@ -95,6 +96,12 @@ def philox(ctr, key, rounds=10):
     out = (C.c_uint32 * 4)()
     load().orc_philox4x32((C.c_uint32 * 4)(*ctr), (C.c_uint32 * 2)(*key), int(rounds), out)
     return list(out)
+
+
+def iteration_key(base, domain, iteration):
+    out = (C.c_uint32 * 2)()
+    load().orc_iteration_key((C.c_uint32 * 2)(*base), int(domain), int(iteration), out)
+    return int(out[0]), int(out[1])
 
 
 def max_threads():

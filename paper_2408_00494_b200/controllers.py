@@ -391,6 +391,7 @@ class Controller:
         self.device = int(device)
         self.stream = stream
         self.last_diagnostics = None
+        self._base = None
         self._dev = None   # created lazily: no CUDA before a fork (sim.py:321-322)
 
     # -- internals
@@ -398,7 +399,13 @@ class Controller:
         return streams.substream(self.seed, *self.run_path, domain, self.iteration)
 
     def _key(self, domain):
-        return _lib.key_arr(streams.device_key(self.seed, *self.run_path, domain, self.iteration))
+        """Per-iteration device key: Philox of (iteration, domain) under the
+        controller's base key (one C call instead of a SeedSequence hash)."""
+        if self._base is None:
+            self._base = _lib.key_arr(streams.base_key(self.seed, *self.run_path))
+        out = (_lib.C.c_uint32 * 2)()
+        _lib.load().bssmppi_iteration_key(self._base, domain, self.iteration, out)
+        return out
 
     def _k_range(self):
         return 0, self.config.samples
@@ -430,11 +437,17 @@ class Controller:
         return eps, z
 
     def _inputs_state(self, state, cov):
-        x0 = np.ascontiguousarray(state, dtype=np.float64).reshape(8)
-        cov0 = None if cov is None else np.ascontiguousarray(cov, dtype=np.float64).reshape(16)
-        plan = np.ascontiguousarray(self.plan.controls, dtype=np.float64)
+        x0 = np.ascontiguousarray(state, dtype=np.float64)
+        if x0.size != 8:
+            raise ValueError("state must have 8 components")
+        cov0 = None if cov is None else np.ascontiguousarray(cov, dtype=np.float64)
+        if cov0 is not None and cov0.size != 16:
+            raise ValueError("cov must be the 4x4 tracked-subset covariance")
+        plan = self.plan.controls
         if plan.shape != (self.config.horizon, CONTROL_DIM):
             raise ValueError("plan shape does not match the horizon")
+        if not (plan.flags.c_contiguous and plan.dtype == np.float64):
+            plan = np.ascontiguousarray(plan, dtype=np.float64)
         return x0, cov0, plan
 
     def _inputs(self, state, cov):

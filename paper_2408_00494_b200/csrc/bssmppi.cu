@@ -713,6 +713,17 @@ int bssmppi_philox4x32(const uint32_t ctr[4], const uint32_t key[2], int32_t rou
   return BSSMPPI_OK;
 }
 
+int bssmppi_iteration_key(const uint32_t base[2], uint32_t domain, uint64_t iteration, uint32_t out[2]) {
+  if (!base || !out) return fail(BSSMPPI_ERR_INVALID, "NULL argument");
+  // Philox4x32-10 of (iteration lo, iteration hi, domain, tag) under the
+  // controller's base key: distinct (domain, iteration) -> independent keys.
+  const Philox4 r = philox4x32<10>(Philox4{(uint32_t)iteration, (uint32_t)(iteration >> 32), domain, 0x6b657973u},
+                                   philox_schedule(base[0], base[1]));
+  out[0] = r.x;
+  out[1] = r.y;
+  return BSSMPPI_OK;
+}
+
 int bssmppi_ffma_peak(int32_t device, double *tflops) {
   if (!tflops) return fail(BSSMPPI_ERR_INVALID, "NULL argument");
   int ndev = 0;

@@ -181,8 +181,10 @@ __device__ __forceinline__ void group_allreduce18(float a[18], int li, float *sl
     cnt = up ? max(cnt - H, 0) : min(cnt, H);                                  \
   }
   // offsets descend from G/2 to 1; level sizes for 18 values: 9, 5, 3, 2, 1
+  BSS_ASSERT(base >= 0);
   if (G == 32) {
     BSS_RS_LEVEL(18, 16) BSS_RS_LEVEL(9, 8) BSS_RS_LEVEL(5, 4) BSS_RS_LEVEL(3, 2) BSS_RS_LEVEL(2, 1)
+    BSS_ASSERT(cnt <= 0 || base < 18);
     if (cnt > 0) slot[base] = a[0];
   } else if (G == 16) {
     BSS_RS_LEVEL(18, 8) BSS_RS_LEVEL(9, 4) BSS_RS_LEVEL(5, 2) BSS_RS_LEVEL(3, 1)
@@ -270,6 +272,7 @@ __device__ __forceinline__ void particle_step(const RollParams &P, int t, int k,
   const int M = P.M;
   float z[7];
   if (ZARR) {
+    BSS_ASSERT(t < P.T && k < P.k_count && m < M);
     const float *zp = P.z_in + (((size_t)t * P.k_count + k) * M + m) * 7;
 #pragma unroll
     for (int j = 0; j < 7; ++j) z[j] = zp[j];
@@ -307,10 +310,15 @@ __device__ __forceinline__ void particle_step(const RollParams &P, int t, int k,
   }
 }
 
+// SHARED_WHEELS: after re-projection every particle's next-step wheel
+// speeds equal the shift's (they depend only on the shared terms), so their
+// sums are identically zero and skipped.
+template <bool SHARED_WHEELS>
 __device__ __forceinline__ void accumulate(float acc[18], const float x[8], const float c[8]) {
   float d[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
+    if (SHARED_WHEELS && (i == 3 || i == 4)) { d[i] = 0.f; continue; }
     d[i] = x[i] - c[i];
     acc[i] += d[i];
   }
@@ -377,10 +385,10 @@ __global__ void __launch_bounds__(kBlockThreads, BSS_MIN_BLOCKS) bss_rollout_ker
     if (has0) particle_step<PERSIST, ZARR>(P, t, k, kg, li, mean, L, ctl, sh, cloud, x);
 #pragma unroll
     for (int i = 0; i < 8; ++i) c[i] = __shfl_sync(0xffffffffu, x[i], 0, G);
-    if (has0) accumulate(acc, x, c);
+    if (has0) accumulate<!PERSIST>(acc, x, c);
     for (int m = li + G; m < M; m += G) {
       particle_step<PERSIST, ZARR>(P, t, k, kg, m, mean, L, ctl, sh, cloud, x);
-      accumulate(acc, x, c);
+      accumulate<!PERSIST>(acc, x, c);
     }
     group_allreduce18<G>(acc, li, slots + (t & 1) * kSlotFloats);
 

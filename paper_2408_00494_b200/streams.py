@@ -33,3 +33,11 @@ def device_key(root_seed: int, *path: int) -> tuple:
     """(k0, k1) uint32 Philox4x32 key for the substream (root_seed, *path)."""
     k = _seed_sequence(root_seed, path).generate_state(2, np.uint32)
     return int(k[0]), int(k[1])
+
+
+def base_key(root_seed: int, *path: int) -> tuple:
+    """Controller base key: SeedSequence(root_seed, spawn_key=path) -- the
+    reference's stream identity (streams.py:21-28) without domain/iteration.
+    Per-iteration keys are derived from it on the host by
+    ``bssmppi_iteration_key`` (Philox4x32-10 of (iteration, domain))."""
+    return device_key(root_seed, *path)

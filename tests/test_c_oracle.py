@@ -69,3 +69,16 @@ def test_philox_mode_thread_invariant():
     a, _ = c_oracle.control_step(prob, inp.x0, None, inp.plan, (1, 2), (3, 4), threads=1)
     b, _ = c_oracle.control_step(prob, inp.x0, None, inp.plan, (1, 2), (3, 4), threads=4)
     np.testing.assert_array_equal(a, b)
+
+
+def test_iteration_key_matches_product_library():
+    """The device-noise key schedule is host code in the product library; the
+    C oracle restates it (used by the CPU closed-loop arm)."""
+    from paper_2408_00494_b200 import _lib
+    lib = _lib.load()
+    out = (_lib.C.c_uint32 * 2)()
+    for base, dom, it in [((1, 2), 2, 0), ((0xDEADBEEF, 7), 3, 12345), ((5, 6), 2, 2 ** 40 + 3)]:
+        assert lib.bssmppi_iteration_key((_lib.C.c_uint32 * 2)(*base), dom, it, out) == 0
+        assert (out[0], out[1]) == c_oracle.iteration_key(base, dom, it)
+    assert c_oracle.iteration_key((1, 2), 2, 0) != c_oracle.iteration_key((1, 2), 3, 0)
+    assert c_oracle.iteration_key((1, 2), 2, 0) != c_oracle.iteration_key((1, 2), 2, 1)

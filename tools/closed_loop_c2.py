@@ -28,8 +28,9 @@ class OracleController:
         self.last_diagnostics = {}
 
     def control_step(self, x):
-        kc = streams.device_key(self.seed, *self.run_path, 2, self.iteration)
-        kb = streams.device_key(self.seed, *self.run_path, 3, self.iteration)
+        base = streams.base_key(self.seed, *self.run_path)
+        kc = self.c.iteration_key(base, 2, self.iteration)
+        kb = self.c.iteration_key(base, 3, self.iteration)
         t0 = time.perf_counter()
         vplus, _ = self.c.control_step(self.prob, x, None, self.plan, kc, kb)
         self.last_diagnostics = {"device_ms": 1e3 * (time.perf_counter() - t0)}
