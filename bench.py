@@ -223,11 +223,18 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # one rank per GPU; BSSMPPI_DIST_BACKEND=gloo lets the N>1 mechanics run
+    # on a single GPU for testing (host-staged all-reduce, no waiting kernels)
+    backend = os.environ.get("BSSMPPI_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
 
     from paper_2408_00494_b200 import _lib, streams
     from paper_2408_00494_b200 import controllers as mc
@@ -236,7 +243,8 @@ def main():
     stream = torch.cuda.current_stream()
     if world > 1:
         from paper_2408_00494_b200.distributed import ShardedController
-        ctrl = ShardedController(cfg, cost, model, track, noise=noise, seed=0, run_path=(5, 0))
+        ctrl = ShardedController(cfg, cost, model, track, noise=noise, seed=0, run_path=(5, 0),
+                                 device=local)
     else:
         ctrl = mc.Controller(cfg, cost, model, track, noise=noise, seed=0, run_path=(5, 0),
                              device=local, stream=stream.cuda_stream)

@@ -202,7 +202,9 @@ void fill_params(bssmppi_ctx *c, const bssmppi_problem *p) {
 // SMs).  The per-(k, t) work (shared step terms, reduction, Cholesky, costs)
 // costs the same warp instructions for 1 or 32/G rollouts, so narrower groups
 // amortise it over more particles (C3: G = 8, 32 particles per lane, -10% vs
-// G = 32).  Depends only on (M, K), never on the shard.
+// G = 32).  Decided on the LOCAL rollout count: a K-shard of 2048 rollouts
+// (C3 over 8 GPUs) keeps one warp per rollout instead of starving the SMs;
+// across world sizes the moment sums may then differ by FP32 summation order.
 #ifndef BSS_MIN_P
 #define BSS_MIN_P 32
 #endif
@@ -233,7 +235,7 @@ cudaError_t launch_bss_g(const RollParams &rp, bool persist, bool zarr, cudaStre
 int launch_rollout(bssmppi_ctx *c, const RollParams &rp, bool zarr) {
   cudaError_t e;
   if (c->kind == BSSMPPI_KIND_BSS) {
-    switch (group_width(rp.M, c->K)) {
+    switch (group_width(rp.M, rp.k_count)) {
       case 2: e = launch_bss_g<2>(rp, c->persist, zarr, c->stream); break;
       case 4: e = launch_bss_g<4>(rp, c->persist, zarr, c->stream); break;
       case 8: e = launch_bss_g<8>(rp, c->persist, zarr, c->stream); break;
