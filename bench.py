@@ -323,7 +323,8 @@ def main():
     if tpath.exists():
         tj = json.loads(tpath.read_text())
         traffic = tj.get(args.workload)
-    roofline = {"bound": "fp32", "kernel": "bss_rollout_kernel<32,false,false>",
+    G = _lib.load().bssmppi_group_width(wl["M"], k_count)
+    roofline = {"bound": "fp32", "kernel": f"bss_rollout_kernel<{G},false,false>",
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak if peak else None,
                 "peak_source": "FFMA microbenchmark measured in this run (MEASURED_PEAKS.json has "

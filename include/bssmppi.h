@@ -105,6 +105,8 @@ const char *bssmppi_last_error(void);
 int32_t bssmppi_abi_version(void);
 /* Size of one K-shard partial record: 5 + 2*horizon doubles. */
 int32_t bssmppi_partial_len(int32_t horizon);
+/* Lanes per rollout the bss kernel uses for (M, local rollout count). */
+int32_t bssmppi_group_width(int32_t inner_samples, int32_t k_count);
 
 int bssmppi_create(const bssmppi_problem *problem, int32_t device, bssmppi_ctx **out);
 void bssmppi_destroy(bssmppi_ctx *ctx);

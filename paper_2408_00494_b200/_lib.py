@@ -65,6 +65,7 @@ SIGNATURES = {
     "bssmppi_last_error": (C.c_char_p, []),
     "bssmppi_abi_version": (C.c_int32, []),
     "bssmppi_partial_len": (C.c_int32, [C.c_int32]),
+    "bssmppi_group_width": (C.c_int32, [C.c_int32, C.c_int32]),
     "bssmppi_create": (C.c_int, [C.POINTER(Problem), C.c_int32, C.POINTER(_ctx)]),
     "bssmppi_destroy": (None, [_ctx]),
     "bssmppi_set_stream": (C.c_int, [_ctx, C.c_void_p]),

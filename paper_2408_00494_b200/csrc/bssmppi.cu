@@ -374,6 +374,10 @@ int32_t bssmppi_abi_version(void) { return BSSMPPI_ABI_VERSION; }
 
 int32_t bssmppi_partial_len(int32_t horizon) { return kRecHead + 2 * horizon; }
 
+int32_t bssmppi_group_width(int32_t inner_samples, int32_t k_count) {
+  return group_width(std::max(2, inner_samples), std::max(1, k_count));
+}
+
 int bssmppi_create(const bssmppi_problem *problem, int32_t device, bssmppi_ctx **out) {
   if (!out) return fail(BSSMPPI_ERR_INVALID, "out is NULL");
   *out = nullptr;

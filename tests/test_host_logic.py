@@ -191,3 +191,15 @@ class TestSharding:
 def test_default_subset():
     assert DEFAULT_SUBSET.indices == (1, 2, 5, 6)
     assert DEFAULT_SUBSET.position(6) == 3
+
+
+def test_group_width_policy():
+    """Lanes per rollout (csrc/bssmppi.cu group_width): one warp for small
+    problems, narrower groups with >= 32 particles per lane once the local
+    rollout count fills two waves."""
+    from paper_2408_00494_b200 import _lib
+    gw = _lib.load().bssmppi_group_width
+    assert gw(32, 256) == 32 and gw(5, 40) == 8 and gw(2, 16) == 2
+    assert gw(256, 16384) == 8          # C3 on one GPU
+    assert gw(256, 2048) == 32          # C3 shard at 8 GPUs
+    assert gw(64, 32768) == 4          # 16 particles per lane (C5 32768 x 64)
