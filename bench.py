@@ -45,22 +45,35 @@ WORKLOADS = {
     "C5_4096x512": dict(K=4096, M=512, T=60, dt=0.04, track="spline0", noise_std=0.05),
     "C5_32768x64": dict(K=32768, M=64, T=60, dt=0.04, track="spline0", noise_std=0.05),
     "C5_131072x256": dict(K=131072, M=256, T=60, dt=0.04, track="spline0", noise_std=0.05),
+    # config 4: extension beyond the reference (obstacles.py): Laplace(0.03) + U(+-0.05) slip,
+    # shield beta = 0.2, 16 seeded obstacles with delta = 0.02 chance constraints
+    "C4": dict(K=65536, M=64, T=50, dt=0.04, track="spline0", noise_std=None, laplace=(0.03, 0.05),
+               cbf_rate=0.2, obstacles=16),
 }
 
 
 def build_problem_objects(wl):
+    """(cfg, cost, model, track, noise, x0, obstacles) of a workload."""
     from paper_2408_00494_b200 import controllers as mc
     from paper_2408_00494_b200 import dynamics as md
+    from paper_2408_00494_b200.constraints import SafetyParams
     from paper_2408_00494_b200.tracks import named_track
 
     track = named_track(wl["track"])
     model = md.with_timestep(md.VehicleParams(), wl["dt"], "euler")
     cfg = mc.MppiConfig(kind="bss", samples=wl["K"], horizon=wl["T"], inner_samples=wl["M"],
                         sigma_eps=np.diag([0.2 ** 2, 0.5 ** 2]))
-    noise = md.NoiseModel(np.diag([wl["noise_std"] ** 2] * 3))
+    obstacles = None
+    if wl.get("laplace"):
+        from paper_2408_00494_b200.obstacles import LaplaceSlipNoise, place_obstacles
+        noise = LaplaceSlipNoise(*wl["laplace"])
+        obstacles = place_obstacles(track, wl["obstacles"], seed=0) if wl.get("obstacles") else None
+    else:
+        noise = md.NoiseModel(np.diag([wl["noise_std"] ** 2] * 3))
+    cost = mc.CostSpec(safety=SafetyParams(wl.get("cbf_rate", 0.35), 2000.0))
     s0 = float(np.random.default_rng(0).uniform(0.0, track.length))
     x0 = md.VehicleState.rolling(5.0, model, s=s0).as_array()
-    return cfg, mc.CostSpec(), model, track, noise, x0
+    return cfg, cost, model, track, noise, x0, obstacles
 
 
 # ----------------------------------------------------------------- clocks
@@ -115,8 +128,8 @@ def cpu_rate(wl, seconds, threads=0, key=(1, 2)):
     from oracle import c_oracle
     from paper_2408_00494_b200.controllers import RolloutContext, build_problem
 
-    cfg, cost, model, track, noise, x0 = build_problem_objects(wl)
-    ctx = RolloutContext(model, track, cost, noise=noise)
+    cfg, cost, model, track, noise, x0, obstacles = build_problem_objects(wl)
+    ctx = RolloutContext(model, track, cost, noise=noise, obstacles=obstacles)
     nthr = threads or c_oracle.max_threads()
     plan = np.zeros((wl["T"], 2))
 
@@ -149,8 +162,8 @@ def reference_arm(args, wl):
     from oracle import c_oracle
     from paper_2408_00494_b200.controllers import RolloutContext, build_problem
 
-    cfg, cost, model, track, noise, x0 = build_problem_objects(wl)
-    ctx = RolloutContext(model, track, cost, noise=noise)
+    cfg, cost, model, track, noise, x0, obstacles = build_problem_objects(wl)
+    ctx = RolloutContext(model, track, cost, noise=noise, obstacles=obstacles)
     nthr = c_oracle.max_threads()
     rate, _, _ = cpu_rate(wl, 0.5)
     k = int(min(wl["K"], max(nthr, rate * args.ref_step_seconds / (wl["M"] * wl["T"]))))
@@ -185,10 +198,15 @@ def reference_arm(args, wl):
 
 
 def workload_config(args, wl):
+    extra = {}
+    if wl.get("laplace"):
+        extra = {"noise": f"Laplace({wl['laplace'][0]}) + U(+-{wl['laplace'][1]}) slip on vy",
+                 "cbf_rate": wl["cbf_rate"], "obstacles": wl["obstacles"],
+                 "extension": "beyond the reference (obstacles.py); parity vs extended C oracle"}
     return {"workload": f"{args.workload}: BSS-MPPI iteration K={wl['K']} x M={wl['M']} x "
                         f"T={wl['T']}, dt={wl['dt']}, track={wl['track']}",
             "K": wl["K"], "M": wl["M"], "T": wl["T"], "dt": wl["dt"], "track": wl["track"],
-            "process_noise_std": wl["noise_std"], "control_noise_std": [0.2, 0.5],
+            "process_noise_std": wl["noise_std"], "control_noise_std": [0.2, 0.5], **extra,
             "global_batch": wl["K"], "seq_len": wl["T"], "parallelism": f"k-shard{args.gpus}",
             "l2": "flushed (256 MiB memset) between timed iterations"}
 
@@ -239,15 +257,15 @@ def main():
     from paper_2408_00494_b200 import _lib, streams
     from paper_2408_00494_b200 import controllers as mc
 
-    cfg, cost, model, track, noise, x0 = build_problem_objects(wl)
+    cfg, cost, model, track, noise, x0, obstacles = build_problem_objects(wl)
     stream = torch.cuda.current_stream()
     if world > 1:
         from paper_2408_00494_b200.distributed import ShardedController
         ctrl = ShardedController(cfg, cost, model, track, noise=noise, seed=0, run_path=(5, 0),
-                                 device=local)
+                                 device=local, obstacles=obstacles)
     else:
         ctrl = mc.Controller(cfg, cost, model, track, noise=noise, seed=0, run_path=(5, 0),
-                             device=local, stream=stream.cuda_stream)
+                             device=local, stream=stream.cuda_stream, obstacles=obstacles)
     k_begin, k_count = ctrl._k_range()
 
     def barrier():

@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define BSSMPPI_ABI_VERSION 1
+#define BSSMPPI_ABI_VERSION 2
 
 typedef enum {
   BSSMPPI_OK = 0,
@@ -86,6 +86,19 @@ typedef struct bssmppi_problem {
   /* K-shard owned by this context: global k in [k_begin, k_begin + k_count) */
   int32_t k_begin;
   int32_t k_count;
+  /* ---- Extensions BEYOND the reference (BASELINE config 4); zero = off.
+   * The reference has only Gaussian noise (dynamics.py:289-290) and only the
+   * track DCBF in its rollouts (controllers.py:293); see obstacles.py. */
+  int32_t noise_kind;            /* 0: Gaussian via noise_factor; 1: Laplace(laplace_scale) on
+                                    (vx, vy, r) + U(-slip_bias, slip_bias) on vy (Philox only) */
+  double laplace_scale;
+  double slip_bias;
+  int32_t n_obstacles;           /* <= 64 */
+  const double *obstacles;       /* n x 3: centre x, y, radius (global frame) */
+  double obstacle_backoff;       /* nu of each obstacle chance constraint (heuristic_h_i) */
+  const double *centerline;      /* rows x 3: x, y, theta at s = i * centerline_ds */
+  int32_t centerline_n;
+  double centerline_ds;
 } bssmppi_problem;
 
 /* Diagnostics of one iteration (the reference returns none; north_star asks). */

@@ -211,6 +211,48 @@ int orc_philox4x32(const uint32_t ctr[4], const uint32_t key[2], int rounds, uin
   return 0;
 }
 
+/* Config-4 extension (beyond the reference; obstacles.py): Laplace + slip
+ * noise from the second Philox block's words, obstacle heuristic terms. */
+static double centred_uniform(uint32_t w) { return ((double)(w >> 9) + 0.5) * (1.0 / 8388608.0) - 0.5; }
+
+static void belief_noise_laplace(uint32_t k0, uint32_t k1, uint32_t t, uint32_t kg, uint32_t m, double b,
+                                 double a, double z[4], double w[3]) {
+  uint32_t p[4] = {t, m, kg, 0u}, q[4] = {t, m, kg, 1u};
+  philox_r(p, k0, k1, 7);
+  philox_r(q, k0, k1, 7);
+  bm(p[0], p[1], &z[0], &z[1]);
+  bm(p[2], p[3], &z[2], &z[3]);
+  for (int i = 0; i < 3; ++i) {
+    double u = centred_uniform(q[i]);
+    w[i] = -b * copysign(log(1.0 - 2.0 * fabs(u)), u);
+  }
+  w[1] += 2.0 * a * centred_uniform(q[3]);
+}
+
+static double obstacle_terms(const bssmppi_problem *p, double s, double ey, double sigy, int *inside) {
+  const double L = p->track_length;
+  double sw = p->track_closed ? pymod(s, L) : fmin(fmax(s, 0.0), L);
+  double fi = sw / p->centerline_ds;
+  int j = (int)fi;
+  if (j < 0) j = 0;
+  if (j > p->centerline_n - 2) j = p->centerline_n - 2;
+  double f = fi - j;
+  const double *a = p->centerline + 3 * j, *b = a + 3;
+  double cx = a[0] + f * (b[0] - a[0]), cy = a[1] + f * (b[1] - a[1]), th = a[2] + f * (b[2] - a[2]);
+  double nx = -sin(th), ny = cos(th);
+  double px = cx + ey * nx, py = cy + ey * ny, h = INFINITY;
+  *inside = 0;
+  for (int i = 0; i < p->n_obstacles; ++i) {
+    const double *o = p->obstacles + 3 * i;
+    double dx = px - o[0], dy = py - o[1], d = sqrt(dx * dx + dy * dy);
+    if (d < o[2]) *inside = 1;
+    double eta = d > 0.0 ? (dx * nx + dy * ny) / d : 1.0;
+    double hi = d - o[2] - p->obstacle_backoff * fabs(eta) * sigy;
+    if (hi < h) h = hi;
+  }
+  return h;
+}
+
 static double stage(const bssmppi_problem *p, const double *x) {
   double quad = 0.0;
   for (int i = 0; i < 8; ++i) {
@@ -247,12 +289,18 @@ static double rollout_one(const Ctx *c, const Inputs *in, int k, double *xs, dou
   const int bss = p->kind == BSSMPPI_KIND_BSS, shield = p->kind != BSSMPPI_KIND_MPPI;
   double sig = bss ? sqrt(fmax(cov[15], 0.0)) : 0.0;
   double h_cur = dcbf(p, mean[6], sig), h_prev = h_cur;
+  int inside = 0;
+  double ho_cur = p->n_obstacles ? obstacle_terms(p, mean[7], mean[6], sig, &inside) : 0.0, ho_prev = ho_cur;
   int noise_on = 0;
   for (int i = 0; i < 9; ++i) noise_on |= p->noise_factor[i] != 0.0;
   const double *F = p->noise_factor;
   for (int t = 0; t < T; ++t) {
     total += stage(p, mean);
     if (shield && t > 0) total += pen(p, h_cur, h_prev);
+    if (p->n_obstacles) {
+      if (inside) total += p->obstacle_penalty;
+      if (shield && t > 0) total += pen(p, ho_cur, ho_prev);
+    }
     double v0 = in->nominal[2 * t], v1 = in->nominal[2 * t + 1], e0, e1, u0, u1;
     const size_t o = ((size_t)k * T + t) * 2;
     if (in->philox_ctrl) {
@@ -275,13 +323,16 @@ static double rollout_one(const Ctx *c, const Inputs *in, int k, double *xs, dou
     if (!bss) {
       dead |= !step_euler(c, mean, u0, u1);
       if (shield) { h_prev = h_cur; h_cur = dcbf(p, mean[6], 0.0); }
+      if (p->n_obstacles) { ho_prev = ho_cur; ho_cur = obstacle_terms(p, mean[7], mean[6], 0.0, &inside); }
       continue;
     }
     const int reproject = !(p->persist_particles && t > 0);
     if (reproject) chol4(cov, L);
     for (int m = 0; m < M; ++m) {
-      double z[7];
-      if (in->philox_belief) belief_normals(in->kb[0], in->kb[1], t, kg, m, z);
+      double z[7] = {0, 0, 0, 0, 0, 0, 0}, wl[3] = {0.0, 0.0, 0.0};
+      if (in->philox_belief && p->noise_kind == 1)
+        belief_noise_laplace(in->kb[0], in->kb[1], t, kg, m, p->laplace_scale, p->slip_bias, z, wl);
+      else if (in->philox_belief) belief_normals(in->kb[0], in->kb[1], t, kg, m, z);
       else {
         const double *zp = in->z_in + (((size_t)t * K + k) * M + m) * 7;
         for (int j = 0; j < 7; ++j) z[j] = zp[j];
@@ -296,7 +347,9 @@ static double rollout_one(const Ctx *c, const Inputs *in, int k, double *xs, dou
         }
       }
       step_euler(c, x, u0, u1);
-      if (noise_on)
+      if (p->noise_kind == 1)
+        for (int i = 0; i < 3; ++i) x[i] += wl[i];
+      else if (noise_on)
         for (int i = 0; i < 3; ++i) x[i] += F[i * 3] * z[4] + F[i * 3 + 1] * z[5] + F[i * 3 + 2] * z[6];
     }
     double mu[8], cv[16];
@@ -310,9 +363,17 @@ static double rollout_one(const Ctx *c, const Inputs *in, int k, double *xs, dou
     dead |= !ok;
     h_prev = h_cur;
     h_cur = dcbf(p, mean[6], sqrt(fmax(cov[15], 0.0)));
+    if (p->n_obstacles) {
+      ho_prev = ho_cur;
+      ho_cur = obstacle_terms(p, mean[7], mean[6], sqrt(fmax(cov[15], 0.0)), &inside);
+    }
   }
   total += p->terminal_scale * stage(p, mean);
   if (shield) total += pen(p, h_cur, h_prev);
+  if (p->n_obstacles) {
+    total += p->terminal_scale * (inside ? p->obstacle_penalty : 0.0);
+    if (shield) total += pen(p, ho_cur, ho_prev);
+  }
   return dead ? INFINITY : total;
 }
 

@@ -42,6 +42,10 @@ class Problem(C.Structure):
         ("track_n", C.c_int32), ("track_length", C.c_double), ("half_width", C.c_double),
         ("track_closed", C.c_int32),
         ("k_begin", C.c_int32), ("k_count", C.c_int32),
+        ("noise_kind", C.c_int32), ("laplace_scale", C.c_double), ("slip_bias", C.c_double),
+        ("n_obstacles", C.c_int32), ("obstacles", C.POINTER(C.c_double)),
+        ("obstacle_backoff", C.c_double), ("centerline", C.POINTER(C.c_double)),
+        ("centerline_n", C.c_int32), ("centerline_ds", C.c_double),
     ]
 
 

@@ -160,6 +160,7 @@ class RolloutContext:
     cost: CostSpec
     noise: NoiseModel = None
     subset: object = field(default_factory=lambda: DEFAULT_SUBSET)
+    obstacles: object = None      # config-4 extension (obstacles.Obstacles), beyond the reference
 
     def __post_init__(self):
         if self.noise is None:
@@ -174,6 +175,8 @@ def _bounds_arrays(bounds):
 
 
 def _check_supported(ctx, cost):
+    if getattr(ctx.noise, "kind", "gaussian") not in ("gaussian", "laplace_slip"):
+        raise NotImplementedError(f"noise kind {ctx.noise.kind!r}")
     sub = tuple(getattr(ctx.subset, "indices", ctx.subset))
     if sub != tuple(DEFAULT_SUBSET.indices):
         raise NotImplementedError(f"device path tracks the default subset {DEFAULT_SUBSET.indices}, got {sub}")
@@ -226,7 +229,26 @@ def build_problem(kind, K, T, M, temperature, gamma, sigma_eps, precision, bound
     p.track_closed = int(bool(ctx.track.closed))
     p.k_begin = int(k_begin)
     p.k_count = int(K - k_begin if k_count is None else k_count)
-    return p, (s, kap)
+    keep = [s, kap]
+    # config-4 extensions (obstacles.py) -- beyond the reference
+    if getattr(ctx.noise, "kind", "gaussian") == "laplace_slip":
+        p.noise_kind = 1
+        p.laplace_scale = float(ctx.noise.scale)
+        p.slip_bias = float(ctx.noise.slip_bias)
+    obst = getattr(ctx, "obstacles", None)
+    if obst is not None and len(obst.radius):
+        from .obstacles import centerline_table
+        arr = np.ascontiguousarray(obst.as_array(), dtype=np.float64)
+        table, ds = centerline_table(ctx.track)
+        table = np.ascontiguousarray(table, dtype=np.float64)
+        p.n_obstacles = arr.shape[0]
+        p.obstacles = _lib.dptr(arr)
+        p.obstacle_backoff = float(obst.backoff)
+        p.centerline = _lib.dptr(table)
+        p.centerline_n = table.shape[0]
+        p.centerline_ds = float(ds)
+        keep += [arr, table]
+    return p, tuple(keep)
 
 
 class DeviceContext:
@@ -369,19 +391,25 @@ class Controller:
 
     Extra keyword-only options (defaults keep the reference call shape):
     ``noise_source`` ("philox" | "reference"), ``device`` (CUDA ordinal),
-    ``stream`` (cudaStream_t as int).  After each ``control_step`` the
+    ``stream`` (cudaStream_t as int), ``obstacles`` (config-4 extension,
+    ``obstacles.Obstacles``; with ``noise=obstacles.LaplaceSlipNoise(...)``
+    this is BASELINE config 4, beyond the reference).  After each ``control_step`` the
     attribute ``last_diagnostics`` holds v+, the cost minimum/argmin, the
     number of finite rollouts, the effective sample size and the device
     time of the iteration.
     """
 
     def __init__(self, config, cost, model, track, noise=None, subset=None, seed: int = 0,
-                 run_path=(), *, noise_source: str = "philox", device: int = 0, stream=None):
+                 run_path=(), *, noise_source: str = "philox", device: int = 0, stream=None,
+                 obstacles=None):
         if noise_source not in NOISE_SOURCES:
             raise ValueError(f"noise_source must be one of {NOISE_SOURCES}")
+        if noise_source == "reference" and getattr(noise, "kind", "gaussian") != "gaussian":
+            raise ValueError("only Gaussian noise has a reference stream; use noise_source='philox'")
         self.config = config
         self.ctx = RolloutContext(model=model, track=track, cost=cost, noise=noise,
-                                  subset=subset if subset is not None else DEFAULT_SUBSET)
+                                  subset=subset if subset is not None else DEFAULT_SUBSET,
+                                  obstacles=obstacles)
         _check_supported(self.ctx, cost)
         self.seed = int(seed)
         self.run_path = tuple(int(p) for p in run_path)

@@ -64,6 +64,7 @@ struct bssmppi_ctx {
   float *d_state = nullptr;   // x0[8] | cov0[16] | plan[2T]
   float *d_u = nullptr, *d_cost = nullptr;
   float4 *d_ctl = nullptr;    // per-(k,t) control table
+  float4 *d_obs = nullptr, *d_cl = nullptr;   // config-4 extension tables
   float *d_cc = nullptr;      // per-(k,t) control-cost terms
   double *d_eps = nullptr, *d_uin = nullptr;
   float *d_z = nullptr, *d_mom = nullptr;
@@ -111,6 +112,35 @@ int validate(const bssmppi_problem *p) {
   if (p->track_closed ? !(p->track_length > p->track_s[p->track_n - 1]) : (p->track_length < p->track_s[p->track_n - 1]))
     return fail(BSSMPPI_ERR_INVALID, "track length inconsistent with samples");
   if (!(p->dt > 0.0)) return fail(BSSMPPI_ERR_INVALID, "dt must be > 0");
+  if (p->noise_kind < 0 || p->noise_kind > 1) return fail(BSSMPPI_ERR_INVALID, "unknown noise kind %d", p->noise_kind);
+  if (p->n_obstacles < 0 || p->n_obstacles > 64) return fail(BSSMPPI_ERR_UNSUPPORTED, "0..64 obstacles supported");
+  if (p->n_obstacles > 0 && (!p->obstacles || !p->centerline || p->centerline_n < 2 || !(p->centerline_ds > 0.0)))
+    return fail(BSSMPPI_ERR_INVALID, "obstacles need a centerline table");
+  return BSSMPPI_OK;
+}
+
+// Config-4 extension tables (obstacles.py).
+int build_extensions(bssmppi_ctx *c, const bssmppi_problem *p) {
+  RollParams &r = c->rp;
+  r.noise_kind = p->noise_kind;
+  r.lap_b = (float)p->laplace_scale;
+  r.slip_a = (float)p->slip_bias;
+  r.n_obs = p->n_obstacles;
+  r.nu_obs = (float)p->obstacle_backoff;
+  if (p->n_obstacles == 0) return BSSMPPI_OK;
+  std::vector<float4> ob(p->n_obstacles), cl(p->centerline_n);
+  for (int i = 0; i < p->n_obstacles; ++i)
+    ob[i] = make_float4((float)p->obstacles[3 * i], (float)p->obstacles[3 * i + 1], (float)p->obstacles[3 * i + 2], 0.f);
+  for (int i = 0; i < p->centerline_n; ++i)
+    cl[i] = make_float4((float)p->centerline[3 * i], (float)p->centerline[3 * i + 1], (float)p->centerline[3 * i + 2], 0.f);
+  int rc;
+  if ((rc = dev_alloc(&c->d_obs, ob.size())) || (rc = dev_alloc(&c->d_cl, cl.size()))) return rc;
+  CUDA_TRY(cudaMemcpy(c->d_obs, ob.data(), ob.size() * sizeof(float4), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(c->d_cl, cl.data(), cl.size() * sizeof(float4), cudaMemcpyHostToDevice));
+  r.obs = c->d_obs;
+  r.cl = c->d_cl;
+  r.cl_n = p->centerline_n;
+  r.cl_inv_ds = (float)(1.0 / p->centerline_ds);
   return BSSMPPI_OK;
 }
 
@@ -319,6 +349,8 @@ int stage_noise(bssmppi_ctx *c, RollParams &rp, const double *eps, const float *
   }
   if (z) {
     if (c->kind != BSSMPPI_KIND_BSS) return fail(BSSMPPI_ERR_INVALID, "belief normals given to a deterministic controller");
+    if (c->rp.noise_kind != 0)
+      return fail(BSSMPPI_ERR_UNSUPPORTED, "Laplace/slip noise has no reference stream (Philox mode only)");
     const size_t n = (size_t)c->T * c->k_count * c->M * 7;
     int rc = ensure(&c->d_z, &c->cap_z, n);
     if (rc) return rc;
@@ -403,6 +435,7 @@ int bssmppi_create(const bssmppi_problem *problem, int32_t device, bssmppi_ctx *
   fill_params(c, problem);
   auto bail = [&](int code) { bssmppi_destroy(c); return code; };
   if ((rc = build_track(c, problem))) return bail(rc);
+  if ((rc = build_extensions(c, problem))) return bail(rc);
   const int T2 = 2 * c->T;
   c->nblocks = std::min(1024, std::max(1, std::min((c->k_count + 63) / 64, 2 * 148)));
   c->chunk = (c->k_count + c->nblocks - 1) / c->nblocks;
@@ -430,7 +463,7 @@ void bssmppi_destroy(bssmppi_ctx *c) {
   DeviceGuard guard(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   cudaFree(c->d_node); cudaFree(c->d_cell); cudaFree(c->d_state); cudaFree(c->d_u);
-  cudaFree(c->d_cost); cudaFree(c->d_ctl); cudaFree(c->d_cc); cudaFree(c->d_eps); cudaFree(c->d_uin); cudaFree(c->d_z);
+  cudaFree(c->d_cost); cudaFree(c->d_ctl); cudaFree(c->d_cc); cudaFree(c->d_obs); cudaFree(c->d_cl); cudaFree(c->d_eps); cudaFree(c->d_uin); cudaFree(c->d_z);
   cudaFree(c->d_mom); cudaFree(c->d_rec); cudaFree(c->d_out);
   if (c->h_state) cudaFreeHost(c->h_state);
   if (c->h_out) cudaFreeHost(c->h_out);

@@ -105,6 +105,30 @@ __device__ __forceinline__ void belief_normals(const PhiloxKeys &rk, uint32_t t,
   box_muller1(b.z, b.w, z[6]);
 }
 
+// Config-4 extension: 4 re-projection normals + Laplace(0, b) on (vx, vy, r)
+// + U(-a, a) lateral slip on vy from the same two Philox4x32-7 blocks (the
+// second block's words become the uniforms instead of Box-Muller normals).
+__device__ __forceinline__ float centred_uniform(uint32_t w) {   // (-0.5, 0.5)
+  return ((float)(w >> 9) + 0.5f) * 1.1920928955078125e-07f - 0.5f;
+}
+
+__device__ __forceinline__ void belief_noise_laplace(const PhiloxKeys &rk, uint32_t t, uint32_t kg,
+                                                     uint32_t m, float b, float a, float z[4],
+                                                     float w[3]) {
+  const Philox4 p = philox4x32<kBeliefRounds>(Philox4{t, m, kg, 0u}, rk);
+  const Philox4 q = philox4x32<kBeliefRounds>(Philox4{t, m, kg, 1u}, rk);
+  box_muller(p.x, p.y, z[0], z[1]);
+  box_muller(p.z, p.w, z[2], z[3]);
+  const uint32_t words[3] = {q.x, q.y, q.z};
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const float u = centred_uniform(words[i]);
+    // inverse CDF: -b sgn(u) ln(1 - 2|u|)
+    w[i] = -b * copysignf(0.69314718056f * __log2f(1.0f - 2.0f * fabsf(u)), u);
+  }
+  w[1] += 2.0f * a * centred_uniform(q.w);
+}
+
 // The 2 standard normals of control sample (k, t) (controllers.py:175).
 __device__ __forceinline__ void control_normals(const PhiloxKeys &rk, uint32_t t, uint32_t kg,
                                                 float &z0, float &z1) {

@@ -58,6 +58,15 @@ struct RollParams {
   float *ccost;          // [k_count*T] per-(k,t) control-cost terms
   float *cost_out;       // [k_count]
   float *mom_out;        // [T*k_count*18] or null
+  // config-4 extensions (obstacles.py); n_obs == 0 and noise_kind == 0 = reference
+  int noise_kind;        // 1: Laplace + uniform vy slip
+  float lap_b, slip_a;
+  int n_obs;
+  const float4 *obs;     // {x, y, radius, 0}
+  float nu_obs;
+  const float4 *cl;      // centerline rows {x, y, theta, 0} at s = i / cl_inv_ds
+  int cl_n;
+  float cl_inv_ds;
 };
 
 __device__ __forceinline__ float stage_cost(const float x[8], const RollParams &P) {
@@ -80,6 +89,36 @@ __device__ __forceinline__ float dcbf(float ey, float sigy, const RollParams &P)
 __device__ __forceinline__ float shield_penalty(float hc, float hp, const RollParams &P) {
   // constraints.py:172-186: C max(-(h_k - (1 - beta) h_{k-1}), 0)
   return P.c_pen * fmaxf(-(hc - P.beta1 * hp), 0.f);
+}
+
+// Obstacle terms of a belief mean (config-4 extension, obstacles.py):
+// p = centerline(s) + e_y n(s); for each obstacle d_i = |p - o_i|,
+// h_i = d_i - r_i - nu |d d_i / d e_y| sigma_y (reference heuristic_h_i,
+// constraints.py:112-120, on the tracked subset), h_obs = min_i h_i;
+// inside = some d_i < r_i (collision indicator of the stage cost).
+__device__ __forceinline__ float obstacle_terms(const RollParams &P, float s, float ey, float sigy,
+                                                bool &inside) {
+  const float sw = P.tr.closed ? floor_mod(s, P.tr.L) : fminf(fmaxf(s, 0.f), P.tr.L);
+  const float fi = sw * P.cl_inv_ds;
+  const int j = min(max((int)fi, 0), P.cl_n - 2);
+  const float f = fi - (float)j;
+  const float4 a = P.cl[j], b = P.cl[j + 1];
+  const float cx = fmaf(f, b.x - a.x, a.x), cy = fmaf(f, b.y - a.y, a.y), th = fmaf(f, b.z - a.z, a.z);
+  float st, ct;
+  sincosf(th, &st, &ct);
+  const float nx = -st, ny = ct;
+  const float px = fmaf(ey, nx, cx), py = fmaf(ey, ny, cy);
+  float h = __int_as_float(0x7f800000);
+  inside = false;
+  for (int i = 0; i < P.n_obs; ++i) {
+    const float4 o = P.obs[i];
+    const float dx = px - o.x, dy = py - o.y;
+    const float d = sqrtf(dx * dx + dy * dy);
+    inside |= d < o.z;
+    const float eta = (d > 0.f) ? (dx * nx + dy * ny) / d : 1.f;
+    h = fminf(h, d - o.z - P.nu_obs * fabsf(eta) * sigy);
+  }
+  return h;
 }
 
 // Per-(k,t) control: sample/clamp/control-cost (controllers.py:166-177, 223-228).
@@ -271,7 +310,10 @@ __device__ __forceinline__ void particle_step(const RollParams &P, int t, int k,
                                               float x[8]) {
   const int M = P.M;
   float z[7];
-  if (ZARR) {
+  float wl[3] = {0.f, 0.f, 0.f};
+  if (!ZARR && P.noise_kind == 1) {
+    belief_noise_laplace(P.kb, (uint32_t)t, (uint32_t)kg, (uint32_t)m, P.lap_b, P.slip_a, z, wl);
+  } else if (ZARR) {
     BSS_ASSERT(t < P.T && k < P.k_count && m < M);
     const float *zp = P.z_in + (((size_t)t * P.k_count + k) * M + m) * 7;
 #pragma unroll
@@ -295,7 +337,11 @@ __device__ __forceinline__ void particle_step(const RollParams &P, int t, int k,
   // shares (vx, omega_f, omega_r, s) with the mean, hence the shared terms
   if (PERSIST && t > 0) vehicle_step(x, ctl, P.V, P.tr);
   else step_particle(x, sh, ctl, P.V, P.tr);
-  if (P.noise_diag) {                    // added after integration (dynamics.py:571-572)
+  if (P.noise_kind == 1) {               // config-4 extension, after integration too
+    x[0] += wl[0];
+    x[1] += wl[1];
+    x[2] += wl[2];
+  } else if (P.noise_diag) {             // added after integration (dynamics.py:571-572)
     x[0] = fmaf(P.F[0], z[4], x[0]);
     x[1] = fmaf(P.F[4], z[5], x[1]);
     x[2] = fmaf(P.F[8], z[6], x[2]);
@@ -365,12 +411,19 @@ __global__ void __launch_bounds__(kBlockThreads, BSS_MIN_BLOCKS) bss_rollout_ker
   chol4(C, L, 4);   // the initial belief covariance is not a sample estimate
   float h_cur = dcbf(mean[6], sqrtf(fmaxf(C[9], 0.f)), P);
   float h_prev = h_cur;
+  bool inside = false;
+  float ho_cur = P.n_obs ? obstacle_terms(P, mean[7], mean[6], sqrtf(fmaxf(C[9], 0.f)), inside) : 0.f;
+  float ho_prev = ho_cur;
   bool dead = false;
   const float4 *ctl_row = P.ctl + (size_t)k * P.T;
 
   for (int t = 0; t < P.T; ++t) {
     total += stage_cost(mean, P);
     if (t > 0) total += shield_penalty(h_cur, h_prev, P);
+    if (P.n_obs) {
+      if (inside) total += P.c_obs;
+      if (t > 0) total += shield_penalty(ho_cur, ho_prev, P);
+    }
     const float4 cv = ctl_row[t];
     const CtlDev ctl{cv.x, cv.y, cv.z, cv.w};
     StepShared sh;
@@ -431,9 +484,14 @@ __global__ void __launch_bounds__(kBlockThreads, BSS_MIN_BLOCKS) bss_rollout_ker
     for (int i = 0; i < 10; ++i) C[i] = isfinite(C[i]) ? C[i] : 0.f;
     h_prev = h_cur;
     h_cur = dcbf(mean[6], sqrtf(fmaxf(C[9], 0.f)), P);
+    if (P.n_obs) {
+      ho_prev = ho_cur;
+      ho_cur = obstacle_terms(P, mean[7], mean[6], sqrtf(fmaxf(C[9], 0.f)), inside);
+    }
     if (!PERSIST) chol4(C, L, P.chol_rank);
   }
   total += P.term * stage_cost(mean, P) + shield_penalty(h_cur, h_prev, P);
+  if (P.n_obs) total += P.term * (inside ? P.c_obs : 0.f) + shield_penalty(ho_cur, ho_prev, P);
   if (active && li == 0) P.cost_out[k] = dead ? __int_as_float(0x7f800000) : total;
 }
 
@@ -450,11 +508,18 @@ __global__ void __launch_bounds__(kBlockThreads) det_rollout_kernel(const RollPa
   for (int i = 0; i < 8; ++i) x[i] = P.x0[i];
   float h_cur = SHIELD ? dcbf(x[6], 0.f, P) : 0.f;
   float h_prev = h_cur;
+  bool inside = false;
+  float ho_cur = P.n_obs ? obstacle_terms(P, x[7], x[6], 0.f, inside) : 0.f;
+  float ho_prev = ho_cur;
   bool dead = false;
   const float4 *ctl_row = P.ctl + (size_t)k * P.T;
   for (int t = 0; t < P.T; ++t) {
     total += stage_cost(x, P);
     if (SHIELD && t > 0) total += shield_penalty(h_cur, h_prev, P);
+    if (P.n_obs) {
+      if (inside) total += P.c_obs;
+      if (SHIELD && t > 0) total += shield_penalty(ho_cur, ho_prev, P);
+    }
     const float4 cv = ctl_row[t];
     const bool ok = vehicle_step(x, CtlDev{cv.x, cv.y, cv.z, cv.w}, P.V, P.tr);
     dead |= !ok;
@@ -462,9 +527,17 @@ __global__ void __launch_bounds__(kBlockThreads) det_rollout_kernel(const RollPa
       h_prev = h_cur;
       h_cur = dcbf(x[6], 0.f, P);
     }
+    if (P.n_obs) {
+      ho_prev = ho_cur;
+      ho_cur = obstacle_terms(P, x[7], x[6], 0.f, inside);
+    }
   }
   total += P.term * stage_cost(x, P);
   if (SHIELD) total += shield_penalty(h_cur, h_prev, P);
+  if (P.n_obs) {
+    total += P.term * (inside ? P.c_obs : 0.f);
+    if (SHIELD) total += shield_penalty(ho_cur, ho_prev, P);
+  }
   P.cost_out[k] = dead ? __int_as_float(0x7f800000) : total;
 }
 

@@ -44,7 +44,7 @@ class ShardedController(Controller):
     state; all ranks return the same (u0, next plan)."""
 
     def __init__(self, config, cost, model, track, noise=None, subset=None, seed: int = 0,
-                 run_path=(), *, group=None, device=None, noise_source: str = "philox"):
+                 run_path=(), *, group=None, device=None, noise_source: str = "philox", obstacles=None):
         import torch
         import torch.distributed as dist
 
@@ -57,7 +57,7 @@ class ShardedController(Controller):
             device = torch.cuda.current_device()
         super().__init__(config, cost, model, track, noise, subset, seed, run_path,
                          noise_source=noise_source, device=device,
-                         stream=torch.cuda.current_stream(device).cuda_stream)
+                         stream=torch.cuda.current_stream(device).cuda_stream, obstacles=obstacles)
         self.partials = torch.zeros((self.world, partial_len(config.horizon)), dtype=torch.float64,
                                     device=f"cuda:{device}")
 

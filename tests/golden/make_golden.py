@@ -154,6 +154,23 @@ def plant_vectors():
     print("plant_rk4: 256 states")
 
 
+def trackframe_vectors():
+    """Reference TrackFrame poses (dynamics.py:592-690) on the BASELINE tracks,
+    for the config-4 centerline table (obstacles.py)."""
+    from paper_2408_00494_b200.tracks import named_track
+    out = {}
+    for name in ("ellipse", "spline0", "oval"):
+        tr = named_track(name, build=rd.make_test_track)
+        fr = rd.TrackFrame(tr)
+        q = np.linspace(0.0, tr.length, 401)[:-1] + 0.0137
+        out[name + "_s"] = q
+        out[name + "_pose"] = np.array([fr.pose(v) for v in q])
+        g = np.array([fr.to_global(v, 0.7, 0.1) for v in q[::10]])
+        out[name + "_global_ey0.7"] = g
+    np.savez_compressed(HERE / "trackframe.npz", **out)
+    print("trackframe: 3 tracks")
+
+
 if __name__ == "__main__":
     os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
     names = set(sys.argv[1:])
@@ -166,3 +183,5 @@ if __name__ == "__main__":
         closed_loop_vectors()
     if not names or "plant" in names:
         plant_vectors()
+    if not names or "trackframe" in names:
+        trackframe_vectors()
