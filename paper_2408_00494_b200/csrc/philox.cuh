@@ -76,10 +76,11 @@ __device__ __forceinline__ float sqrt_approx(float x) {
 // insertion (no I2F on the XU pipe): u1 in (0, 1], angle in [-pi, pi).
 __device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float &z0, float &z1) {
   const float u1 = 2.0f - __uint_as_float(0x3f800000u | (a >> 9));
-  const float u2 = __uint_as_float(0x3f800000u | (b >> 9)) - 1.5f;
+  // angle 2 pi (m - 1.5) for the mantissa value m in [1, 2): one FFMA
+  const float ang = fmaf(__uint_as_float(0x3f800000u | (b >> 9)), 6.28318530718f, -9.42477796077f);
   const float r = sqrt_approx(-1.38629436112f * __log2f(u1));  // sqrt(-2 ln u1)
   float s, c;
-  __sincosf(6.28318530718f * u2, &s, &c);
+  __sincosf(ang, &s, &c);
   z0 = r * c;
   z1 = r * s;
 }
@@ -87,9 +88,9 @@ __device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float &z0, fl
 // Single normal (cosine branch) of a Box-Muller pair.
 __device__ __forceinline__ void box_muller1(uint32_t a, uint32_t b, float &z0) {
   const float u1 = 2.0f - __uint_as_float(0x3f800000u | (a >> 9));
-  const float u2 = __uint_as_float(0x3f800000u | (b >> 9)) - 1.5f;
+  const float ang = fmaf(__uint_as_float(0x3f800000u | (b >> 9)), 6.28318530718f, -9.42477796077f);
   const float r = sqrt_approx(-1.38629436112f * __log2f(u1));
-  z0 = r * __cosf(6.28318530718f * u2);
+  z0 = r * __cosf(ang);
 }
 
 // The 7 standard normals of particle-step (t, k, m) (Philox4x32-7 counters): [0:4] re-projection
