@@ -98,8 +98,11 @@ __device__ __forceinline__ float curvature(const TrackDev &tr, float s) {
 }
 
 // Non-finite components -> 0 (dynamics.py:493-496); returns "all finite".
-__device__ __noinline__ bool scrub_nonfinite(float *x) {
+// Inlined into the cold branch: an out-of-line call taking x by address
+// would pin the particle state in local memory for the whole loop.
+__device__ __forceinline__ bool scrub_nonfinite(float *x) {
   bool fin = true;
+#pragma unroll
   for (int i = 0; i < 8; ++i) {
     fin &= isfinite(x[i]);
     x[i] = isfinite(x[i]) ? x[i] : 0.f;
