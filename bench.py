@@ -35,6 +35,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 FLOP_PER_PARTICLE_STEP = 162      # SURVEY.md 8d algorithmic FP32 FLOP (FMA = 2)
+SFU_PER_PARTICLE_STEP = 16         # SURVEY.md 8d algorithmic transcendental evaluations
 METRIC = "belief rollout-steps/s (K*M*T/s)"
 UNIT = "rollout-steps/s"
 
@@ -342,16 +343,31 @@ def main():
         tj = json.loads(tpath.read_text())
         traffic = tj.get(args.workload)
     G = _lib.load().bssmppi_group_width(wl["M"], k_count)
-    roofline = {"bound": "fp32", "kernel": f"bss_rollout_kernel<{G},false,false>",
-                "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak if peak else None,
-                "peak_source": "FFMA microbenchmark measured in this run (MEASURED_PEAKS.json has "
-                               "no FP32 figure); nominal 148 SM x 128 FMA x 2 x sm_max_mhz = "
-                               f"{nominal:.1f} TFLOP/s",
-                "frac_of_nominal": achieved / nominal, "traffic": traffic,
+    fp32 = {"achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak if peak else None,
+            "peak_source": "FFMA microbenchmark measured in this run (MEASURED_PEAKS.json has "
+                           "no FP32 figure); nominal 148 SM x 128 FMA x 2 x sm_max_mhz = "
+                           f"{nominal:.1f} TFLOP/s",
+            "frac_of_nominal": achieved / nominal,
+            "algorithmic_flop_per_launch": flop, "flop_per_particle_step": FLOP_PER_PARTICLE_STEP}
+    sfu_ops = SFU_PER_PARTICLE_STEP * k_count * wl["M"] * wl["T"]
+    sfu_achieved = sfu_ops / (roll_avg * 1e-3) / 1e12
+    sfu_peak = ctypes_mufu_peak(_lib, local)
+    sfu = {"achieved": sfu_achieved, "peak": sfu_peak, "unit": "Tops/s",
+           "frac": sfu_achieved / sfu_peak if sfu_peak else None,
+           "peak_source": "MUFU ex2.approx microbenchmark measured in this run; nominal "
+                          "148 SM x 16 x sm_max_mhz = "
+                          f"{nominal / 16:.2f} Tops/s",
+           "algorithmic_ops_per_launch": sfu_ops, "ops_per_particle_step": SFU_PER_PARTICLE_STEP}
+    # the reported fraction is the binding one of FP32 / SFU /
+    # HBM (HBM is < 1 % here: 70 KB of DRAM traffic per launch)
+    bind = sfu if (sfu["frac"] or 0) > (fp32["frac"] or 0) else fp32
+    roofline = {"bound": "sfu" if bind is sfu else "fp32",
+                "kernel": f"bss_rollout_kernel<{G},false,false>",
+                "achieved": bind["achieved"], "peak": bind["peak"], "unit": bind["unit"],
+                "frac": bind["frac"], "traffic": traffic,
                 "rollout_ms": roll_avg, "rollout_share_of_step": roll_avg / statistics.mean(step_ms),
-                "algorithmic_flop_per_launch": flop,
-                "flop_per_particle_step": FLOP_PER_PARTICLE_STEP}
+                "fp32": fp32, "sfu": sfu}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -378,6 +394,12 @@ def main():
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def ctypes_mufu_peak(_lib, device):
+    out = _lib.C.c_double(0.0)
+    _lib.check(_lib.load().bssmppi_mufu_peak(device, _lib.C.byref(out)))
+    return out.value
 
 
 def ctypes_ffma_peak(_lib, device):

@@ -207,6 +207,10 @@ int bssmppi_iteration_key(const uint32_t base[2], uint32_t domain, uint64_t iter
 /* Measured FP32 FFMA throughput of the device (roofline denominator). */
 int bssmppi_ffma_peak(int32_t device, double *tflops);
 
+/* Measured MUFU (XU pipe, ex2.approx) throughput of the device in Tera
+ * ops/s: the denominator of the transcendental (SFU) roofline. */
+int bssmppi_mufu_peak(int32_t device, double *tops);
+
 #ifdef __cplusplus
 }
 #endif

@@ -92,6 +92,7 @@ SIGNATURES = {
     "bssmppi_philox4x32": (C.c_int, [_u32p, _u32p, C.c_int32, _u32p]),
     "bssmppi_belief_normals": (C.c_int, [_u32p, C.c_int32, C.c_int32, C.c_int32, _fp]),
     "bssmppi_ffma_peak": (C.c_int, [C.c_int32, _dp]),
+    "bssmppi_mufu_peak": (C.c_int, [C.c_int32, _dp]),
     "bssmppi_iteration_key": (C.c_int, [_u32p, C.c_uint32, C.c_uint64, _u32p]),
 }
 

@@ -668,6 +668,25 @@ __global__ void __launch_bounds__(256) ffma_peak_kernel(float *out, int iters, f
   if (s == 12345.678f) out[0] = s;
 }
 
+// MUFU (XU pipe) throughput: 8 independent ex2.approx chains per thread,
+// x <- 2^(-x) stays in (0.5, 1); the negation is a free operand modifier.
+__global__ void __launch_bounds__(256) mufu_peak_kernel(float *out, int iters) {
+  float x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = 0.5f + threadIdx.x * 1e-4f + i * 1e-2f;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(x[i]) : "f"(-x[i]));
+    }
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += x[i];
+  if (s == 12345.678f) out[0] = s;
+}
+
 __global__ void philox_kernel(Philox4 c, uint32_t k0, uint32_t k1, int rounds, uint32_t *out) {
   const PhiloxKeys rk = philox_schedule(k0, k1);
   const Philox4 r = rounds == 7 ? philox4x32<7>(c, rk) : philox4x32<10>(c, rk);
@@ -792,6 +811,38 @@ int bssmppi_ffma_peak(int32_t device, double *tflops) {
   if (e != cudaSuccess) return fail(BSSMPPI_ERR_CUDA, "ffma_peak: %s", cudaGetErrorString(e));
   const double flops = 2.0 * 8 * 16 * (double)iters * blocks * 256;
   *tflops = flops / (ms * 1e-3) / 1e12;
+  return BSSMPPI_OK;
+}
+
+int bssmppi_mufu_peak(int32_t device, double *tops) {
+  if (!tops) return fail(BSSMPPI_ERR_INVALID, "NULL argument");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+    return fail(BSSMPPI_ERR_CUDA, "no CUDA device %d", device);
+  DeviceGuard guard(device);
+  cudaSetDevice(device);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  float *d = nullptr;
+  int rc = dev_alloc(&d, 1);
+  if (rc) return rc;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int blocks = sms * 8, iters = 512;
+  mufu_peak_kernel<<<blocks, 256>>>(d, 16);   // warm-up
+  cudaEventRecord(e0);
+  mufu_peak_kernel<<<blocks, 256>>>(d, iters);
+  cudaEventRecord(e1);
+  cudaError_t e = cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(BSSMPPI_ERR_CUDA, "mufu_peak: %s", cudaGetErrorString(e));
+  const double ops = 8.0 * 16 * (double)iters * blocks * 256;
+  *tops = ops / (ms * 1e-3) / 1e12;
   return BSSMPPI_OK;
 }
 
