@@ -206,6 +206,10 @@ void fill_params(bssmppi_ctx *c, const bssmppi_problem *p) {
   V.rrf = (float)(q[19] * q[21] * q[4]); V.rrr = (float)(q[19] * q[22] * q[4]);
   V.spin_scale = (float)(q[4] / 0.1); V.dt = (float)p->dt;
   V.mf_poly = (std::max(std::max(q[7], q[9]), std::max(q[11], q[13])) <= 1.3) ? 1 : 0;
+  V.lf_nlr = make_float2(V.lf, -V.lr);
+  V.By_s = make_float2(V.Byf, -V.Byr);
+  V.Cy = make_float2(V.Cyf, V.Cyr);
+  V.Dy = make_float2(V.Dyf, V.Dyr);
   RollParams &r = c->rp;
   r.k_count = p->k_count; r.k_begin = p->k_begin; r.T = p->horizon; r.M = std::max(1, p->inner_samples);
   r.invM = (float)(1.0 / r.M);

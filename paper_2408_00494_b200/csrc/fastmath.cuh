@@ -66,6 +66,61 @@ __device__ __forceinline__ void sincos_pi(float x, float &s, float &c) {
   c = fmaf(q, t, 1.0f);
 }
 
+// ---- packed FP32x2 forms (sm_100 FFMA2/FMUL2/FADD2: two IEEE lanes per
+// issue slot, each lane rounded exactly like the scalar instruction).
+
+__device__ __forceinline__ float2 bc2(float v) { return make_float2(v, v); }
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// atan of two arguments: a = min(|x|, 1/|x|) in [0, 1], atan(a) = a + a s P(s)
+// with s = a^2 (degree-7 minimax in s, tools/fit_poly.py atan: 1.9 ulp on
+// the whole line), pi/2 - atan(a) for |x| > 1, sign of x.  inf -> +-pi/2.
+__device__ __forceinline__ float2 atan_x2(float2 x) {
+  const float tx = fabsf(x.x), ty = fabsf(x.y);
+  const float2 a = make_float2(fminf(tx, rcp_approx(tx)), fminf(ty, rcp_approx(ty)));
+  const float2 s = __fmul2_rn(a, a);
+  float2 p = __ffma2_rn(s, bc2(2.920688828e-03f), bc2(-1.636791416e-02f));
+  p = __ffma2_rn(p, s, bc2(4.321184009e-02f));
+  p = __ffma2_rn(p, s, bc2(-7.552212477e-02f));
+  p = __ffma2_rn(p, s, bc2(1.066600382e-01f));
+  p = __ffma2_rn(p, s, bc2(-1.421105564e-01f));
+  p = __ffma2_rn(p, s, bc2(1.999377310e-01f));
+  p = __ffma2_rn(p, s, bc2(-3.333315253e-01f));
+  p = __fmul2_rn(p, s);
+  p = __ffma2_rn(a, p, a);
+  const float2 q = __fadd2_rn(bc2(1.57079637f), make_float2(-p.x, -p.y));
+  return make_float2(copysignf(tx > 1.f ? q.x : p.x, x.x), copysignf(ty > 1.f ? q.y : p.y, x.y));
+}
+
+// sin and cos of one argument in one packed Horner chain: lane x runs the
+// sine polynomial (padded with a leading 0, so it is evaluated exactly as
+// the scalar Horner), lane y the cosine; coefficients as in sincos_pi.
+__constant__ float2 kSinCosPi[9] = {
+    {0.0f, 4.101670311e-14f},           {-6.416872784e-13f, -1.134152147e-11f},
+    {1.582333015e-10f, 2.086320672e-09f}, {-2.502759777e-08f, -2.755647870e-07f},
+    {2.755584774e-06f, 2.480155672e-05f}, {-1.984121918e-04f, -1.388888806e-03f},
+    {8.333332837e-03f, 4.166666791e-02f}, {-1.666666716e-01f, -5.0e-01f},
+    {1.0f, 1.0f}};
+
+// returns (sin x, cos x), any x (reduced to [-pi, pi] as in sincos_pi)
+__device__ __forceinline__ float2 sincos_pi_x2(float x) {
+  if (fabsf(x) > 3.14159265f) {
+    const float n = rintf(x * 0.159154943f);
+    x = fmaf(-n, 6.28318548e+00f, x);
+    x = fmaf(n, 1.74845553e-07f, x);
+  }
+  const float t = x * x;
+  float2 p = kSinCosPi[0];
+#pragma unroll
+  for (int j = 1; j < 9; ++j) p = __ffma2_rn(p, bc2(t), kSinCosPi[j]);
+  return make_float2(p.x * x, p.y);
+}
+
 // atan2(y, x) given r = 1/x (x != 0, already computed by the caller):
 // atan(y r) in the right half plane, +-pi shifted in the left one.
 __device__ __forceinline__ float atan2_rcp(float y, float x, float r) {

@@ -36,6 +36,10 @@ struct VehDev {
   float Dxf, Dyf, Dxr, Dyr;
   float drive, vfloor, rrf, rrr, spin_scale, dt;
   int mf_poly;   // all magic-formula C <= 1.3: angles fit sin_mf/cos_mf's range
+  // front/rear lane pairs of the packed (FFMA2) particle step
+  float2 lf_nlr;   // (lf, -lr)
+  float2 By_s;     // (Byf, -Byr): B alpha with alpha_r = -atan2(.) folded in
+  float2 Cy, Dy;   // (Cyf, Cyr), (Dyf, Dyr)
 };
 
 // node[j] = {s_j, kappa_j, slope_j, s_{j+1}} plus a sentinel node[n].
@@ -127,10 +131,14 @@ __device__ __forceinline__ bool all_finite8(const float x[8]) {
 // is the composition, so every path computes bit-identical values.
 struct StepShared {
   float vxe, rx, inv_den;     // low-speed-floored vx and its reciprocal
-  float fxf, fxr, cxf, cxr;   // longitudinal forces and |cos| friction-ellipse factors
+  float fxf, fxr;             // longitudinal forces
+  float2 cx;                  // (front, rear) |cos| friction-ellipse factors
   float dvx_lon;              // (fxr) / m: rear longitudinal force term of dvx
   float wf1, wr1;             // next-step wheel speeds (omega + dt * d omega)
   float kap;                  // kappa(s)
+  float2 fb0;                 // (fxf cd + fxr, fxf sd): the particle-independent
+                              //   parts of the body-frame force sums
+  float2 nsd_cd;              // (-sin delta, cos delta)
 };
 
 __device__ __forceinline__ StepShared step_shared(const float x[8], const CtlDev &c, const VehDev &V,
@@ -151,27 +159,29 @@ __device__ __forceinline__ StepShared step_shared(const float x[8], const CtlDev
   const float txf = V.Cxf * atanf(V.Bxf * sgf), txr = V.Cxr * atanf(V.Bxr * sgr);
   float sxf, sxr;
 #if defined(BSS_EXACT_MATH)
-  sincosf(txf, &sxf, &h.cxf);
-  sincosf(txr, &sxr, &h.cxr);
+  sincosf(txf, &sxf, &h.cx.x);
+  sincosf(txr, &sxr, &h.cx.y);
 #elif defined(BSS_POLY_TIRE)
   if (V.mf_poly) {
-    sxf = sin_mf(txf); h.cxf = cos_mf(txf);
-    sxr = sin_mf(txr); h.cxr = cos_mf(txr);
+    sxf = sin_mf(txf); h.cx.x = cos_mf(txf);
+    sxr = sin_mf(txr); h.cx.y = cos_mf(txr);
   } else {
-    sincosf(txf, &sxf, &h.cxf);
-    sincosf(txr, &sxr, &h.cxr);
+    sincosf(txf, &sxf, &h.cx.x);
+    sincosf(txr, &sxr, &h.cx.y);
   }
 #else
   // MUFU sin/cos (|error| ~3.6e-7 on |theta| <= 2.05): same parity as the
   // polynomial in the harness at less cost
-  __sincosf(txf, &sxf, &h.cxf);
-  __sincosf(txr, &sxr, &h.cxr);
+  __sincosf(txf, &sxf, &h.cx.x);
+  __sincosf(txr, &sxr, &h.cx.y);
 #endif
-  h.cxf = fabsf(h.cxf);
-  h.cxr = fabsf(h.cxr);
+  h.cx.x = fabsf(h.cx.x);
+  h.cx.y = fabsf(h.cx.y);
   h.fxf = V.Dxf * sxf;
   h.fxr = V.Dxr * sxr;
   h.dvx_lon = h.fxr;
+  h.fb0 = make_float2(fmaf(h.fxf, c.cd, h.fxr), h.fxf * c.sd);
+  h.nsd_cd = make_float2(-c.sd, c.cd);
   // _derivs_row wheel torque balance; rolling resistance opposes the spin
 #ifdef BSS_EXACT_MATH
   const float spf = tanhf(wf * V.spin_scale), spr = tanhf(wr * V.spin_scale);
@@ -189,27 +199,16 @@ __device__ __forceinline__ StepShared step_shared(const float x[8], const CtlDev
 // One Euler step x <- x + dt f(x, u), wraps, non-finite -> 0, given the
 // shared terms of x.  Returns the reference's per-particle ok (frame > 0
 // and finite).
+#ifdef BSS_EXACT_MATH
+// libdevice reference form (A/B parity builds, build_cuda(exact=True)).
 __device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, const CtlDev &c,
                                               const VehDev &V, const TrackDev &tr) {
   const float vx = x[0], vy = x[1], r = x[2], ep = x[5], ey = x[6], s = x[7];
-#ifdef BSS_EXACT_MATH
   const float af = c.delta - atan2f(vy + V.lf * r, h.vxe);
   const float ar = -atan2f(vy - V.lr * r, h.vxe);
-#else
-  const float af = c.delta - atan2_rcp(vy + V.lf * r, h.vxe, h.rx);
-  const float ar = -atan2_rcp(vy - V.lr * r, h.vxe, h.rx);
-#endif
   const float tyf = V.Cyf * atanf(V.Byf * af), tyr = V.Cyr * atanf(V.Byr * ar);
-  float syf, syr;
-#if defined(BSS_EXACT_MATH)
-  syf = sinf(tyf); syr = sinf(tyr);
-#elif defined(BSS_POLY_TIRE)
-  if (V.mf_poly) { syf = sin_mf(tyf); syr = sin_mf(tyr); }
-  else { syf = sinf(tyf); syr = sinf(tyr); }
-#else
-  syf = __sinf(tyf); syr = __sinf(tyr);
-#endif
-  const float fyf = V.Dyf * syf * h.cxf, fyr = V.Dyr * syr * h.cxr;
+  const float syf = sinf(tyf), syr = sinf(tyr);
+  const float fyf = V.Dyf * syf * h.cx.x, fyr = V.Dyr * syr * h.cx.y;
   // _derivs_row
   const float fxb = h.fxf * c.cd - fyf * c.sd;
   const float fyb = h.fxf * c.sd + fyf * c.cd;
@@ -220,17 +219,8 @@ __device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, c
   bool ok = frame > 0.f;
   if (frame < 1e-3f) frame = 1e-3f;
   float se, ce;
-#ifdef BSS_EXACT_MATH
   sincosf(ep, &se, &ce);
   const float ds = (vx * ce - vy * se) / frame;
-#else
-#ifdef BSS_MUFU_HEADING
-  __sincosf(ep, &se, &ce);
-#else
-  sincos_pi(ep, se, ce);   // (a warp-vote fast path for small headings measured 7% slower)
-#endif
-  const float ds = __fdividef(vx * ce - vy * se, frame);   // frame in [1e-3, 1 + kappa w]
-#endif
   const float dey = vx * se + vy * ce;
   const float dep = r - h.kap * ds;
   // _step_kernel Euler branch + wraps
@@ -246,6 +236,61 @@ __device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, c
   if (__builtin_expect(!all_finite8(x), 0)) ok = scrub_nonfinite(x) && ok;
   return ok;
 }
+
+#else
+// Packed form of the same step: the front/rear pairs (slip-angle arguments,
+// both arctangent chains, lateral forces), the heading sin/cos polynomials
+// and the (vx, vy) / (e_psi, e_y) Euler updates run as FP32x2 lanes, one
+// issue slot per pair.  Every lane is an IEEE FMA/MUL/ADD, so all kernels
+// (which share this function) stay bit-identical to one another.
+__device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, const CtlDev &c,
+                                              const VehDev &V, const TrackDev &tr) {
+  const float vx = x[0], vy = x[1], r = x[2], ep = x[5], ey = x[6], s = x[7];
+  // slip-angle numerators (vy + lf r, vy - lr r); atan2(., vxe) = atan(. / vxe)
+  // for vxe > 0, +-pi shifted for vxe < 0 (vxe is shared by the rollout)
+  const float2 Y = __ffma2_rn(bc2(r), V.lf_nlr, bc2(vy));
+  float2 A = atan_x2(__fmul2_rn(Y, bc2(h.rx)));
+  if (h.vxe < 0.f) {
+    A.x += copysignf(3.14159265358979f, Y.x);
+    A.y += copysignf(3.14159265358979f, Y.y);
+  }
+  // (B_f alpha_f, B_r alpha_r), alpha_f = delta - A.x, alpha_r = -A.y
+  const float2 ty = __fmul2_rn(V.Cy, atan_x2(__fmul2_rn(V.By_s, make_float2(c.delta - A.x, A.y))));
+  const float2 fy = __fmul2_rn(__fmul2_rn(V.Dy, make_float2(__sinf(ty.x), __sinf(ty.y))), h.cx);
+  // body-frame front force + rear longitudinal: (fxf cd - fyf sd + fxr, fxf sd + fyf cd)
+  const float2 fb = __ffma2_rn(bc2(fy.x), h.nsd_cd, h.fb0);
+  // (dvx, dvy) = (fb.x, fb.y + fyr) / m + (vy r, -vx r)
+  const float2 dv = __ffma2_rn(make_float2(fb.x, fb.y + fy.y), bc2(V.inv_m), make_float2(vy * r, -(vx * r)));
+  const float dr = (V.lf * fb.y - V.lr * fy.y) * V.inv_iz;
+  float frame = 1.f - h.kap * ey;
+  bool ok = frame > 0.f;
+  if (frame < 1e-3f) frame = 1e-3f;
+#ifdef BSS_MUFU_HEADING
+  float2 sc;
+  __sincosf(ep, &sc.x, &sc.y);
+#else
+  const float2 sc = sincos_pi_x2(ep);          // (sin e_psi, cos e_psi)
+#endif
+  const float2 vsc = __fmul2_rn(bc2(vy), sc);  // (vy se, vy ce)
+  const float ds = __fdividef(fmaf(vx, sc.y, -vsc.x), frame);   // frame in [1e-3, 1 + kappa w]
+  const float dey = fmaf(vx, sc.x, vsc.y);
+  const float dep = fmaf(-h.kap, ds, r);
+  // _step_kernel Euler branch + wraps
+  const float2 v01 = __ffma2_rn(bc2(V.dt), dv, make_float2(vx, vy));
+  const float2 v56 = __ffma2_rn(bc2(V.dt), make_float2(dep, dey), make_float2(ep, ey));
+  x[0] = v01.x;
+  x[1] = v01.y;
+  x[2] = fmaf(V.dt, dr, r);
+  x[3] = h.wf1;
+  x[4] = h.wr1;
+  x[5] = wrap_pi(v56.x);
+  x[6] = v56.y;
+  const float s1 = fmaf(V.dt, ds, s);
+  x[7] = tr.closed ? floor_mod(s1, tr.L) : fminf(fmaxf(s1, 0.f), tr.L);
+  if (__builtin_expect(!all_finite8(x), 0)) ok = scrub_nonfinite(x) && ok;
+  return ok;
+}
+#endif
 
 __device__ __forceinline__ bool vehicle_step(float x[8], const CtlDev &c, const VehDev &V,
                                              const TrackDev &tr) {

@@ -64,3 +64,46 @@ def test_sincos_pi():
 def test_magic_formula_angle_bound():
     # C * atan(.) stays inside sin_mf's range for the default C = 1.3
     assert 1.3 * np.pi / 2 < 2.05
+
+
+def _atan_x2_coeffs():
+    body = SRC[SRC.index("float2 atan_x2"):]
+    body = body[:body.index("\n}\n")]
+    first = re.findall(r"bc2\(([-0-9.e+]+)f\)", body)
+    return [np.float32(float(v)) for v in first[:8]]
+
+
+def test_atan_x2():
+    """Packed arctangent (slip angles and lateral magic formula): the
+    device algorithm in float32 with the kernel's Horner order, <= 2 ulp /
+    1.7e-7 absolute on the whole line (libdevice atanf is specified at 2 ulp)."""
+    import sys
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent / "tools"))
+    from fit_poly import atan32
+    c = np.array(_atan_x2_coeffs(), dtype=np.float64)
+    assert len(c) == 8
+    x = np.concatenate([np.linspace(-40, 40, 400001), np.geomspace(1e-6, 1e6, 100001),
+                        -np.geomspace(1e-6, 1e6, 1001), [0.0, np.inf, -np.inf]])
+    x = x.astype(np.float32).astype(np.float64)
+    y = atan32(c, x)
+    ex = np.arctan(x)
+    e = np.abs(y - ex)
+    assert e.max() < 1.7e-7, e.max()
+    ulp = np.spacing(np.abs(ex).astype(np.float32)).astype(np.float64)
+    assert (e / ulp).max() <= 2.0
+    assert np.all(np.sign(y) == np.sign(x))
+
+
+def test_sincos_pi_x2_table_is_the_scalar_polynomials():
+    """The packed (sin, cos) Horner table holds exactly the scalar
+    sincos_pi coefficients (sine padded with a leading 0, which the FMA
+    passes through exactly), so both forms round identically."""
+    body = SRC[SRC.index("kSinCosPi[9] = {"):]
+    body = body[:body.index("};")]
+    pairs = re.findall(r"\{([-0-9.e+]+)f, ([-0-9.e+]+)f\}", body)
+    assert len(pairs) == 9
+    sin_c = [np.float32(float(a)) for a, _ in pairs]
+    cos_c = [np.float32(float(b)) for _, b in pairs]
+    assert sin_c[0] == 0.0
+    assert sin_c[1:] == _coeffs("void sincos_pi")
+    assert cos_c == _coeffs("void sincos_pi", "q")

@@ -1,0 +1,112 @@
+"""Fit the bounded-range polynomials of csrc/fastmath.cuh.
+
+Lawson's algorithm (iteratively re-weighted least squares converging to the
+weighted minimax fit) in float64, coefficients rounded to float32, then the
+float32 Horner evaluation (with FMA, emulated exactly in float64) checked
+on a dense grid.  tests/test_fastmath.py pins the resulting error bounds.
+
+    python tools/fit_poly.py atan      # atan(a) = a + a s P(s), s = a^2, a in [0, 1]
+    python tools/fit_poly.py sin_mf    # sin(x) = x P(x^2), |x| <= 2.05
+    python tools/fit_poly.py cos_mf    # cos(x) = P(x^2),   |x| <= 2.05
+    python tools/fit_poly.py sincos_pi # sin/cos on [-pi, pi]
+"""
+
+import sys
+
+import numpy as np
+
+
+def lawson(basis, target, weight, iters=400):
+    """min_c max_i |weight_i (basis_i . c - target_i)| via Lawson re-weighting."""
+    w = np.full(len(target), 1.0 / len(target))
+    c = None
+    for _ in range(iters):
+        sw = np.sqrt(w) * weight
+        c, *_ = np.linalg.lstsq(basis * sw[:, None], target * sw, rcond=None)
+        err = np.abs(weight * (basis @ c - target))
+        w = w * err
+        w /= w.sum()
+    return c
+
+
+def f32(x):
+    return np.asarray(x, dtype=np.float64).astype(np.float32).astype(np.float64)
+
+
+def fma32(a, b, c):
+    # a*b is exact in float64 for float32 inputs; one rounding to float32
+    return f32(a * b + c)
+
+
+def horner32(coef, t):
+    p = np.full_like(t, coef[0])
+    for ci in coef[1:]:
+        p = fma32(p, t, ci)
+    return p
+
+
+def fit_atan(deg=7):
+    """P of degree ``deg`` in s = a^2 with atan(a) ~= a + a s P(s) on [0, 1];
+    weights make the fit minimax in the relative error of atan."""
+    a = np.cos(np.linspace(np.pi / 2, 0, 20001)) ** 0.5   # dense near 0 and 1
+    a = a[a > 1e-4]
+    s = a * a
+    g = (np.arctan(a) / a - 1.0) / s
+    wt = a * s / np.arctan(a)
+    basis = np.stack([s ** k for k in range(deg, -1, -1)], axis=1)
+    c = f32(lawson(basis, g, wt))
+    return c
+
+
+def atan32(coef, x):
+    """Device algorithm: a = min(|x|, 1/|x|), p = a + a s P(s), pi/2 - p for
+    |x| > 1, sign of x.  MUFU.RCP is modelled as a correctly rounded
+    reciprocal (the hardware's is within 1 ulp)."""
+    t = np.abs(x)
+    with np.errstate(divide="ignore"):
+        r = f32(1.0 / t)
+    a = np.minimum(t, r)
+    s = f32(a * a)
+    p = horner32(coef, s)
+    p = f32(p * s)
+    p = fma32(a, p, a)
+    p = np.where(t > 1.0, f32(np.float32(1.57079637) - p), p)
+    return np.copysign(p, x)
+
+
+def check_atan(coef):
+    x = f32(np.concatenate([np.linspace(-40, 40, 2000001), np.geomspace(1e-6, 1e6, 400001)]))
+    y = atan32(coef, x)
+    ex = np.arctan(x)
+    ulp = np.spacing(np.abs(ex).astype(np.float32)).astype(np.float64)
+    e = np.abs(y - ex)
+    return e.max(), (e / ulp).max()
+
+
+def main():
+    what = sys.argv[1] if len(sys.argv) > 1 else "atan"
+    if what == "atan":
+        for deg in (6, 7):
+            c = fit_atan(deg)
+            abs_e, ulps = check_atan(c)
+            print(f"degree {deg}: max abs err {abs_e:.3e}, {ulps:.2f} ulp")
+            print("  coefficients (highest first):", ", ".join(f"{v:.9e}f" for v in c))
+    else:
+        x = {"sin_mf": 2.05, "cos_mf": 2.05, "sincos_pi": np.pi}[what]
+        xs = np.linspace(1e-4, x, 20001)
+        t = xs * xs
+        for name, odd, deg in (("sin", True, 6 if what == "sin_mf" else 7),
+                               ("cos", False, 7 if what == "cos_mf" else 8)):
+            if what == "sin_mf" and not odd or what == "cos_mf" and odd:
+                continue
+            g = np.sin(xs) / xs if odd else np.cos(xs)
+            basis = np.stack([t ** k for k in range(deg, -1, -1)], axis=1)
+            c = f32(lawson(basis, g, np.ones_like(g)))
+            y = horner32(c, f32(t)) * (xs if odd else 1.0)
+            ref = np.sin(xs) if odd else np.cos(xs)
+            print(f"{name}: max abs err {np.abs(y - ref).max():.3e}")
+            print("  coefficients (highest first):", ", ".join(f"{v:.9e}f" for v in c))
+
+
+if __name__ == "__main__":
+    main()

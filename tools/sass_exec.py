@@ -48,6 +48,32 @@ def main():
         if v < 0.5:
             break
         print(f"  {v:7.2f}  {k}")
+    # stall samples (all samples, per reason), by reason and by source line
+    reasons = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
+    idx = {h: hdr.index(h) for h in reasons}
+    tot = collections.Counter()
+    line_r = collections.defaultdict(collections.Counter)
+    for j, r in enumerate(body):
+        src = ins[j][2] if j < len(ins) else "?"
+        for h, i in idx.items():
+            try:
+                v = float(r[i])
+            except ValueError:
+                continue
+            tot[h] += v
+            line_r[src][h] += v
+    allv = sum(tot.values())
+    print("stall samples by reason:")
+    for h, v in tot.most_common():
+        if v > 0:
+            print(f"  {100 * v / allv:5.1f}%  {h}")
+    print("stall samples by source line (non-selected reasons):")
+    busy = {k: sum(v for h, v in c.items() if h not in ("stall_selected", "stall_not_selected"))
+            for k, c in line_r.items()}
+    for k, v in sorted(busy.items(), key=lambda kv: -kv[1])[:40]:
+        top = ", ".join(f"{h[6:]} {100 * n / allv:.1f}" for h, n in line_r[k].most_common(3)
+                        if h not in ("stall_selected", "stall_not_selected"))
+        print(f"  {100 * v / allv:5.1f}%  {k:24s} {top}")
 
 
 if __name__ == "__main__":
