@@ -72,13 +72,21 @@ __device__ __forceinline__ float sqrt_approx(float x) {
   return y;
 }
 
+// MUFU.LG2 without __log2f's denormal guard (FSETP/FMUL/FADD): the
+// uniforms here are >= 2^-23, never denormal, so the value is identical.
+__device__ __forceinline__ float lg2_approx(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // Box-Muller pair from two 32-bit words.  Uniforms are built by bit
 // insertion (no I2F on the XU pipe): u1 in (0, 1], angle in [-pi, pi).
 __device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float &z0, float &z1) {
   const float u1 = 2.0f - __uint_as_float(0x3f800000u | (a >> 9));
   // angle 2 pi (m - 1.5) for the mantissa value m in [1, 2): one FFMA
   const float ang = fmaf(__uint_as_float(0x3f800000u | (b >> 9)), 6.28318530718f, -9.42477796077f);
-  const float r = sqrt_approx(-1.38629436112f * __log2f(u1));  // sqrt(-2 ln u1)
+  const float r = sqrt_approx(-1.38629436112f * lg2_approx(u1));  // sqrt(-2 ln u1)
   float s, c;
   __sincosf(ang, &s, &c);
   z0 = r * c;
@@ -89,7 +97,7 @@ __device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float &z0, fl
 __device__ __forceinline__ void box_muller1(uint32_t a, uint32_t b, float &z0) {
   const float u1 = 2.0f - __uint_as_float(0x3f800000u | (a >> 9));
   const float ang = fmaf(__uint_as_float(0x3f800000u | (b >> 9)), 6.28318530718f, -9.42477796077f);
-  const float r = sqrt_approx(-1.38629436112f * __log2f(u1));
+  const float r = sqrt_approx(-1.38629436112f * lg2_approx(u1));
   z0 = r * __cosf(ang);
 }
 
@@ -125,7 +133,7 @@ __device__ __forceinline__ void belief_noise_laplace(const PhiloxKeys &rk, uint3
   for (int i = 0; i < 3; ++i) {
     const float u = centred_uniform(words[i]);
     // inverse CDF: -b sgn(u) ln(1 - 2|u|)
-    w[i] = -b * copysignf(0.69314718056f * __log2f(1.0f - 2.0f * fabsf(u)), u);
+    w[i] = -b * copysignf(0.69314718056f * lg2_approx(1.0f - 2.0f * fabsf(u)), u);
   }
   w[1] += 2.0f * a * centred_uniform(q.w);
 }

@@ -114,11 +114,27 @@ __device__ __forceinline__ bool scrub_nonfinite(float *x) {
   return fin;
 }
 
-// Fast screen: a sum of finite values is finite unless it overflows (then
-// the caller's per-component slow path decides); inf/NaN always propagate.
+// Fast screen: max |x_i| with NaN propagation (sm_100 three-input
+// FMNMX3.NAN on the ALU pipe, abs as a free operand modifier) is finite iff
+// every component is.
+__device__ __forceinline__ float max3_nan(float a, float b, float c) {
+  float d;
+  asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+__device__ __forceinline__ float max2_nan(float a, float b) {
+  float d;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+  return d;
+}
+
 __device__ __forceinline__ bool all_finite8(const float x[8]) {
-  const float s = ((x[0] + x[1]) + (x[2] + x[3])) + ((x[4] + x[5]) + (x[6] + x[7]));
-  return fabsf(s) < __int_as_float(0x7f800000);
+  float m = max3_nan(fabsf(x[0]), fabsf(x[1]), fabsf(x[2]));
+  m = max3_nan(m, fabsf(x[3]), fabsf(x[4]));
+  m = max3_nan(m, fabsf(x[5]), fabsf(x[6]));
+  m = max2_nan(m, fabsf(x[7]));
+  return m < __int_as_float(0x7f800000);
 }
 
 // The step split in two: everything that depends only on (vx, omega_f,
@@ -272,7 +288,8 @@ __device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, c
   const float2 sc = sincos_pi_x2(ep);          // (sin e_psi, cos e_psi)
 #endif
   const float2 vsc = __fmul2_rn(bc2(vy), sc);  // (vy se, vy ce)
-  const float ds = __fdividef(fmaf(vx, sc.y, -vsc.x), frame);   // frame in [1e-3, 1 + kappa w]
+  // frame in [1e-3, 1 + kappa w]: MUFU.RCP without __fdividef's huge-divisor guard
+  const float ds = fmaf(vx, sc.y, -vsc.x) * rcp_approx(frame);
   const float dey = fmaf(vx, sc.x, vsc.y);
   const float dep = fmaf(-h.kap, ds, r);
   // _step_kernel Euler branch + wraps
