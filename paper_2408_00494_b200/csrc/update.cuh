@@ -15,6 +15,8 @@ namespace bss {
 
 constexpr int kRecHead = 5;   // beta, Z, Z2, n_finite, argmin
 constexpr int kUpdThreads = 256;
+constexpr int kCombineSlices = 16;    // record slices per column in combine_kernel
+constexpr int kCombinePart = 2048;    // slice partials held in shared memory (16 KB)
 
 __device__ __forceinline__ double to_d(float v) { return (double)v; }
 __device__ __forceinline__ double to_d(double v) { return v; }
@@ -113,6 +115,7 @@ combine_kernel(int nrec, int T2, const double *rec, double lam, int final_, doub
                double lo0, double lo1, double hi0, double hi1, double *vplus, float *plan_out,
                double *head_out) {
   __shared__ double s_scale[1024];
+  __shared__ double s_part[kCombinePart];
   __shared__ double s_a[kUpdThreads], s_b[kUpdThreads], s_c[kUpdThreads];
   __shared__ long long s_i[kUpdThreads];
   __shared__ double s_head[kRecHead];
@@ -165,12 +168,25 @@ combine_kernel(int nrec, int T2, const double *rec, double lam, int final_, doub
     s_head[4] = (double)argmin;
   }
   __syncthreads();
-  // 3. N[col] = sum_r scale_r N_r[col] (records with n_r = 0 carry N_r = 0)
-  for (int col = tid; col < T2; col += kUpdThreads) {
+  // 3. N[col] = sum_r scale_r N_r[col] (records with n_r = 0 carry N_r = 0):
+  //    (column, record-slice) items over all threads -- consecutive threads
+  //    read consecutive columns of one record -- then the slice partials are
+  //    summed in slice order (fixed order: deterministic).
+  const int ns = max(1, min(kCombineSlices, min(kCombinePart / T2, nrec)));
+  const int per = (nrec + ns - 1) / ns;
+  for (int it = tid; it < ns * T2; it += kUpdThreads) {
+    const int col = it % T2, sl = it / T2;
+    const int r0 = sl * per, r1 = min(nrec, r0 + per);
     const double *src = rec + kRecHead + col;
     double a = 0.0;
-#pragma unroll 8
-    for (int r = 0; r < nrec; ++r) a = fma(s_scale[r], src[(size_t)r * R], a);
+#pragma unroll 4
+    for (int r = r0; r < r1; ++r) a = fma(s_scale[r], src[(size_t)r * R], a);
+    s_part[it] = a;
+  }
+  __syncthreads();
+  for (int col = tid; col < T2; col += kUpdThreads) {
+    double a = 0.0;
+    for (int sl = 0; sl < ns; ++sl) a += s_part[sl * T2 + col];
     if (!final_) {
       rec_out[kRecHead + col] = a;
     } else {
