@@ -104,14 +104,26 @@ __device__ __forceinline__ void box_muller1(uint32_t a, uint32_t b, float &z0) {
 // The 7 standard normals of particle-step (t, k, m) (Philox4x32-7 counters): [0:4] re-projection
 // on the tracked subset, [4:7] process noise -- the column layout of the
 // reference's z_all block (controllers.py:285-287, belief.py:328-333).
-__device__ __forceinline__ void belief_normals(const PhiloxKeys &rk, uint32_t t, uint32_t kg,
-                                               uint32_t m, float z[7]) {
-  const Philox4 a = philox4x32<kBeliefRounds>(Philox4{t, m, kg, 0u}, rk);
-  const Philox4 b = philox4x32<kBeliefRounds>(Philox4{t, m, kg, 1u}, rk);
+// The two Philox4x32-7 blocks of particle-step (t, k, m); both noise kinds
+// (Gaussian, config-4 Laplace) transform the same eight words.
+__device__ __forceinline__ void belief_bits(const PhiloxKeys &rk, uint32_t t, uint32_t kg, uint32_t m,
+                                            Philox4 &a, Philox4 &b) {
+  a = philox4x32<kBeliefRounds>(Philox4{t, m, kg, 0u}, rk);
+  b = philox4x32<kBeliefRounds>(Philox4{t, m, kg, 1u}, rk);
+}
+
+__device__ __forceinline__ void normals_from_bits(const Philox4 &a, const Philox4 &b, float z[7]) {
   box_muller(a.x, a.y, z[0], z[1]);
   box_muller(a.z, a.w, z[2], z[3]);
   box_muller(b.x, b.y, z[4], z[5]);
   box_muller1(b.z, b.w, z[6]);
+}
+
+__device__ __forceinline__ void belief_normals(const PhiloxKeys &rk, uint32_t t, uint32_t kg,
+                                               uint32_t m, float z[7]) {
+  Philox4 a, b;
+  belief_bits(rk, t, kg, m, a, b);
+  normals_from_bits(a, b, z);
 }
 
 // Config-4 extension: 4 re-projection normals + Laplace(0, b) on (vx, vy, r)
@@ -121,11 +133,8 @@ __device__ __forceinline__ float centred_uniform(uint32_t w) {   // (-0.5, 0.5)
   return ((float)(w >> 9) + 0.5f) * 1.1920928955078125e-07f - 0.5f;
 }
 
-__device__ __forceinline__ void belief_noise_laplace(const PhiloxKeys &rk, uint32_t t, uint32_t kg,
-                                                     uint32_t m, float b, float a, float z[4],
-                                                     float w[3]) {
-  const Philox4 p = philox4x32<kBeliefRounds>(Philox4{t, m, kg, 0u}, rk);
-  const Philox4 q = philox4x32<kBeliefRounds>(Philox4{t, m, kg, 1u}, rk);
+__device__ __forceinline__ void laplace_from_bits(const Philox4 &p, const Philox4 &q, float b, float a,
+                                                  float z[4], float w[3]) {
   box_muller(p.x, p.y, z[0], z[1]);
   box_muller(p.z, p.w, z[2], z[3]);
   const uint32_t words[3] = {q.x, q.y, q.z};

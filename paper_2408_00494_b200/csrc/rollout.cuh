@@ -260,7 +260,7 @@ constexpr int kBlockThreads = 128;
 // Register budget: 5 resident 128-thread blocks per SM (<= 102 registers,
 // 20 warps/SM) measured fastest at C3 (96 vs 113 registers: -2%).
 #ifndef BSS_MIN_BLOCKS
-#define BSS_MIN_BLOCKS 5
+#define BSS_MIN_BLOCKS 4
 #endif
 
 // Group-wide sum over G lanes (xor butterfly; every lane gets the total).
@@ -301,26 +301,42 @@ __device__ __forceinline__ float control_prologue(const RollParams &P, int k, in
   return cc;
 }
 
-// One particle-step: re-project (or load the persistent particle), Euler
-// step, process noise.  Returns the post-step state in x.
-template <bool PERSIST, bool ZARR>
-__device__ __forceinline__ void particle_step(const RollParams &P, int t, int k, int kg, int m,
-                                              const float mean[8], const float L[10],
-                                              const CtlDev &ctl, const StepShared &sh, float *cloud,
-                                              float x[8]) {
-  const int M = P.M;
-  float z[7];
-  float wl[3] = {0.f, 0.f, 0.f};
-  if (!ZARR && P.noise_kind == 1) {
-    belief_noise_laplace(P.kb, (uint32_t)t, (uint32_t)kg, (uint32_t)m, P.lap_b, P.slip_a, z, wl);
-  } else if (ZARR) {
-    BSS_ASSERT(t < P.T && k < P.k_count && m < M);
-    const float *zp = P.z_in + (((size_t)t * P.k_count + k) * M + m) * 7;
+// The 7 noise values of particle-step (t, k, m): [0:4] the re-projection
+// normals on the tracked subset, [4:7] the process noise -- standard
+// normals scaled by F after the step (the column layout of the reference's
+// z_all block, controllers.py:285-287, belief.py:328-333) or, for the
+// config-4 extension, the Laplace + slip increments themselves.  ZARR reads
+// the reference's normals (zeros past M, where the pipelined loop looks
+// one particle ahead).
+// NK: noise kind (0 Gaussian, 1 Laplace + slip) as a template parameter, so
+// the pipelined loop body is one scheduling region.
+template <bool ZARR, int NK>
+__device__ __forceinline__ void particle_noise(const RollParams &P, int t, int k, int kg, int m, float n[7]) {
+  if (ZARR) {
+    if (m < P.M) {
+      BSS_ASSERT(t < P.T && k < P.k_count);
+      const float *zp = P.z_in + (((size_t)t * P.k_count + k) * P.M + m) * 7;
 #pragma unroll
-    for (int j = 0; j < 7; ++j) z[j] = zp[j];
+      for (int j = 0; j < 7; ++j) n[j] = zp[j];
+    } else {
+#pragma unroll
+      for (int j = 0; j < 7; ++j) n[j] = 0.f;
+    }
   } else {
-    belief_normals(P.kb, (uint32_t)t, (uint32_t)kg, (uint32_t)m, z);
+    Philox4 a, b;
+    belief_bits(P.kb, (uint32_t)t, (uint32_t)kg, (uint32_t)m, a, b);
+    if (NK == 1) laplace_from_bits(a, b, P.lap_b, P.slip_a, n, n + 4);
+    else normals_from_bits(a, b, n);
   }
+}
+
+// One particle-step given its noise: re-project (or load the persistent
+// particle), Euler step, process noise.  Returns the post-step state in x.
+template <bool PERSIST, int NK>
+__device__ __forceinline__ void particle_step(const RollParams &P, int t, int m, const float mean[8],
+                                              const float L[10], const CtlDev &ctl, const StepShared &sh,
+                                              float *cloud, const float z[7], float x[8]) {
+  const int M = P.M;
   if (PERSIST && t > 0) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) x[i] = cloud[i * M + m];
@@ -337,10 +353,10 @@ __device__ __forceinline__ void particle_step(const RollParams &P, int t, int k,
   // shares (vx, omega_f, omega_r, s) with the mean, hence the shared terms
   if (PERSIST && t > 0) vehicle_step(x, ctl, P.V, P.tr);
   else step_particle(x, sh, ctl, P.V, P.tr);
-  if (P.noise_kind == 1) {               // config-4 extension, after integration too
-    x[0] += wl[0];
-    x[1] += wl[1];
-    x[2] += wl[2];
+  if (NK == 1) {                         // config-4 extension, after integration too
+    x[0] += z[4];
+    x[1] += z[5];
+    x[2] += z[6];
   } else if (P.noise_diag) {             // added after integration (dynamics.py:571-572)
     x[0] = fmaf(P.F[0], z[4], x[0]);
     x[1] = fmaf(P.F[4], z[5], x[1]);
@@ -376,6 +392,38 @@ __device__ __forceinline__ void accumulate(float acc[18], const float x[8], cons
   acc[16] = fmaf(a5, a6, acc[16]); acc[17] = fmaf(a6, a6, acc[17]);
 }
 
+// All particles of rollout k at step t for one lane (m = li, li + G, ...):
+// noise, step, and the shifted one-pass moment sums.  Particle 0 of the
+// group doubles as the shift c of the moments: it sits O(sigma) from the
+// mean, and a zero-spread cloud gives d == 0.
+//
+// Software-pipelined noise: the Philox blocks and Box-Muller transforms of
+// particle m + G are produced inside particle m's iteration, so the
+// quarter-rate IMAD.WIDE / MUFU work overlaps the FP32 dynamics in one
+// scheduling region (one extra noise draw per lane and step).
+template <int G, bool PERSIST, bool ZARR, int NK>
+__device__ __forceinline__ void particle_pass(const RollParams &P, int t, int k, int kg, int li,
+                                              const float mean[8], const float L[10], const CtlDev &ctl,
+                                              const StepShared &sh, float *cloud, float acc[18],
+                                              float c[8]) {
+  const int M = P.M;
+  const bool has0 = li < M;
+  float x[8], zc[7], zn[7];
+  particle_noise<ZARR, NK>(P, t, k, kg, li, zc);
+  particle_noise<ZARR, NK>(P, t, k, kg, li + G, zn);
+  if (has0) particle_step<PERSIST, NK>(P, t, li, mean, L, ctl, sh, cloud, zc, x);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) c[i] = __shfl_sync(0xffffffffu, x[i], 0, G);
+  if (has0) accumulate<!PERSIST>(acc, x, c);
+  for (int m = li + G; m < M; m += G) {
+#pragma unroll
+    for (int j = 0; j < 7; ++j) zc[j] = zn[j];
+    particle_noise<ZARR, NK>(P, t, k, kg, m + G, zn);
+    particle_step<PERSIST, NK>(P, t, m, mean, L, ctl, sh, cloud, zc, x);
+    accumulate<!PERSIST>(acc, x, c);
+  }
+}
+
 // BSS rollouts.  G: lanes per rollout; PERSIST: keep the particle cloud in
 // shared memory instead of re-projecting (controllers.py:288-305);
 // ZARR: read the reference's normals instead of Philox.
@@ -396,8 +444,6 @@ __global__ void __launch_bounds__(kBlockThreads, BSS_MIN_BLOCKS) bss_rollout_ker
   float *cloud = PERSIST ? smem + (kBlockThreads / 32) * GPW * 2 * kSlotFloats +
                                (size_t)(warp * GPW + gi) * 8 * P.M
                          : nullptr;
-  const int M = P.M;
-  const bool has0 = li < M;                              // lane owns particle m = li
 
   float total = control_prologue<G>(P, k, kg, li, active);
   float mean[8], C[10], L[10];
@@ -429,20 +475,14 @@ __global__ void __launch_bounds__(kBlockThreads, BSS_MIN_BLOCKS) bss_rollout_ker
     StepShared sh;
     if (!(PERSIST && t > 0)) sh = step_shared(mean, ctl, P.V, P.tr);
 
-    // Particle 0 of the group doubles as the shift of the one-pass moments:
-    // it sits O(sigma) from the mean, and a zero-spread cloud gives d == 0.
     float acc[18];
 #pragma unroll
     for (int i = 0; i < 18; ++i) acc[i] = 0.f;
-    float x[8], c[8];
-    if (has0) particle_step<PERSIST, ZARR>(P, t, k, kg, li, mean, L, ctl, sh, cloud, x);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) c[i] = __shfl_sync(0xffffffffu, x[i], 0, G);
-    if (has0) accumulate<!PERSIST>(acc, x, c);
-    for (int m = li + G; m < M; m += G) {
-      particle_step<PERSIST, ZARR>(P, t, k, kg, m, mean, L, ctl, sh, cloud, x);
-      accumulate<!PERSIST>(acc, x, c);
-    }
+    float c[8];
+    if (!ZARR && P.noise_kind == 1)
+      particle_pass<G, PERSIST, ZARR, 1>(P, t, k, kg, li, mean, L, ctl, sh, cloud, acc, c);
+    else
+      particle_pass<G, PERSIST, ZARR, 0>(P, t, k, kg, li, mean, L, ctl, sh, cloud, acc, c);
     group_allreduce18<G>(acc, li, slots + (t & 1) * kSlotFloats);
 
     // moments (belief.py:275-308 semantics)

@@ -78,8 +78,11 @@ update_partials_kernel(int n, int k_begin, int T2, const CT *costs, const UT *u,
     for (int j = 0; j < 4; ++j) {
       const int col = tid + j * kUpdThreads;
       if (col < T2) {
+        // 8 loads in flight per thread (each is an L2 round trip)
         double a = nacc[j];
-        for (int i = 0; i < cnt_k; ++i) a = fma(s_w[i], to_d(u[(size_t)(base + i) * T2 + col]), a);
+        const UT *up = u + (size_t)base * T2 + col;
+#pragma unroll 8
+        for (int i = 0; i < cnt_k; ++i) a = fma(s_w[i], to_d(up[(size_t)i * T2]), a);
         nacc[j] = a;
       }
     }
