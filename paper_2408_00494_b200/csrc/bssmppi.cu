@@ -13,6 +13,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -231,21 +232,29 @@ void fill_params(bssmppi_ctx *c, const bssmppi_problem *p) {
 }
 
 // Lanes per rollout.  Start from one warp (or the power of two >= M), then
-// narrow the group while each lane would own < BSS_MIN_P particles and the
-// GLOBAL rollout count still fills the device (>= 2 waves of 20 warps x 148
-// SMs).  The per-(k, t) work (shared step terms, reduction, Cholesky, costs)
-// costs the same warp instructions for 1 or 32/G rollouts, so narrower groups
-// amortise it over more particles (C3: G = 8, 32 particles per lane, -10% vs
-// G = 32).  Decided on the LOCAL rollout count: a K-shard of 2048 rollouts
-// (C3 over 8 GPUs) keeps one warp per rollout instead of starving the SMs;
+// narrow the group -- the per-(k, t) work (shared step terms, reduction,
+// Cholesky, costs) costs the same warp instructions for 1 or 32/G rollouts,
+// so narrower groups amortise it over more particles per lane -- as long as
+// the narrower grid keeps the SMs busy:
+//   (1) to >= 8 particles per lane while >= 1024 warps remain;
+//   (2) to <= 64 particles per lane while >= 4096 warps remain (~1.7 waves
+//       of 16 warps x 148 SMs).
+// Fitted to a G sweep over 14 (K, M) shapes with the pipelined kernel
+// (tools/g_sweep.sh, profiles/r1_group_width_sweep.txt): it picks the best
+// or a tied G on every one.  Decided on the LOCAL rollout count, so a
+// K-shard of 2048 rollouts (C3 over 8 GPUs) keeps one warp per rollout;
 // across world sizes the moment sums may then differ by FP32 summation order.
-#ifndef BSS_MIN_P
-#define BSS_MIN_P 32
-#endif
 int group_width(int M, int K) {
+  static const int forced = [] {   // tuning override (tools/g_sweep.py); 0 = policy
+    const char *e = std::getenv("BSSMPPI_FORCE_G");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (forced == 2 || forced == 4 || forced == 8 || forced == 16 || forced == 32) return forced;
   int g = 2;
   while (g < M && g < 32) g <<= 1;
-  while (g > 4 && M < BSS_MIN_P * g && (long long)K * g / 32 >= 2LL * 148 * 20) g >>= 1;
+  const auto warps = [K](int gg) { return (long long)K * gg / 32; };
+  while (g > 4 && M < 8 * g && warps(g / 2) >= 1024) g >>= 1;
+  while (g > 4 && M < 64 * g && warps(g / 2) >= 4096) g >>= 1;
   return g;
 }
 

@@ -195,11 +195,18 @@ def test_default_subset():
 
 def test_group_width_policy():
     """Lanes per rollout (csrc/bssmppi.cu group_width): one warp for small
-    problems, narrower groups with >= 32 particles per lane once the local
-    rollout count fills two waves."""
+    problems; >= 8 particles per lane while >= 1024 warps remain, then up to
+    64 per lane while >= 4096 warps remain -- the measured best G on every
+    swept shape (profiles/r1_group_width_sweep.txt)."""
     from paper_2408_00494_b200 import _lib
     gw = _lib.load().bssmppi_group_width
     assert gw(32, 256) == 32 and gw(5, 40) == 8 and gw(2, 16) == 2
     assert gw(256, 16384) == 8          # C3 on one GPU
+    assert gw(256, 8192) == 16          # C3 shard at 2 GPUs
     assert gw(256, 2048) == 32          # C3 shard at 8 GPUs
-    assert gw(64, 32768) == 4          # 16 particles per lane (C5 32768 x 64)
+    assert gw(256, 32768) == 4          # 64 particles per lane
+    assert gw(64, 32768) == 4           # C5 32768 x 64
+    assert gw(64, 4096) == 8            # C5 4096 x 64: 8 particles per lane
+    assert gw(128, 4096) == 16          # C2
+    assert gw(512, 4096) == 32 and gw(512, 32768) == 8
+    assert gw(64, 65536) == 4           # C4
