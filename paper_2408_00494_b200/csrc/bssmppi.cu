@@ -211,6 +211,8 @@ void fill_params(bssmppi_ctx *c, const bssmppi_problem *p) {
   V.By_s = make_float2(V.Byf, -V.Byr);
   V.Cy = make_float2(V.Cyf, V.Cyr);
   V.Dy = make_float2(V.Dyf, V.Dyr);
+  V.Bx = make_float2(V.Bxf, V.Bxr);
+  V.Cx = make_float2(V.Cxf, V.Cxr);
   RollParams &r = c->rp;
   r.k_count = p->k_count; r.k_begin = p->k_begin; r.T = p->horizon; r.M = std::max(1, p->inner_samples);
   r.invM = (float)(1.0 / r.M);

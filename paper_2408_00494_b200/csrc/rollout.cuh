@@ -155,6 +155,14 @@ __device__ __forceinline__ void control_at(const RollParams &P, int k, int kg, i
 // like the reference's 1e-300 clamp -- and, because a sample covariance of
 // M particles has rank <= M - 1, at most M - 1 pivots are kept (for M <= 4
 // the FP64 reference's extra pivots are rounding noise of O(1e-8 sigma)).
+// sqrt(p) and 1/sqrt(p) of a positive pivot from one MUFU.RSQ (the non-ftz
+// approx form keeps denormal pivots; relative error ~2^-22, far below the
+// FP32 sample-covariance noise) instead of IEEE sqrtf + division.
+__device__ __forceinline__ void pivot_root(float p, float &l, float &inv) {
+  asm("rsqrt.approx.f32 %0, %1;" : "=f"(inv) : "f"(p));
+  l = p * inv;
+}
+
 __device__ __forceinline__ void chol4(const float C[10], float L[10], int max_rank) {
   // packed lower: L00 L10 L11 L20 L21 L22 L30 L31 L32 L33
   // C packed upper: c00 c01 c02 c03 c11 c12 c13 c22 c23 c33
@@ -164,8 +172,8 @@ __device__ __forceinline__ void chol4(const float C[10], float L[10], int max_ra
   float l00 = 0.f, l10 = 0.f, l20 = 0.f, l30 = 0.f;
   if (c00 > 0.f && rank < max_rank) {
     ++rank;
-    l00 = sqrtf(c00);
-    const float inv = 1.f / l00;
+    float inv;
+    pivot_root(c00, l00, inv);
     l10 = c01 * inv; l20 = c02 * inv; l30 = c03 * inv;
   }
   float l11 = 0.f, l21 = 0.f, l31 = 0.f;
@@ -173,8 +181,8 @@ __device__ __forceinline__ void chol4(const float C[10], float L[10], int max_ra
     const float acc = c11 - l10 * l10;
     if (acc > 0.f && rank < max_rank) {
       ++rank;
-      l11 = sqrtf(acc);
-      const float inv = 1.f / l11;
+      float inv;
+      pivot_root(acc, l11, inv);
       l21 = (c12 - l20 * l10) * inv;
       l31 = (c13 - l30 * l10) * inv;
     }
@@ -184,14 +192,18 @@ __device__ __forceinline__ void chol4(const float C[10], float L[10], int max_ra
     const float acc = c22 - l20 * l20 - l21 * l21;
     if (acc > 0.f && rank < max_rank) {
       ++rank;
-      l22 = sqrtf(acc);
-      l32 = (c23 - l30 * l20 - l31 * l21) / l22;
+      float inv;
+      pivot_root(acc, l22, inv);
+      l32 = (c23 - l30 * l20 - l31 * l21) * inv;
     }
   }
   float l33 = 0.f;
   {
     const float acc = c33 - l30 * l30 - l31 * l31 - l32 * l32;
-    if (acc > 0.f && rank < max_rank) l33 = sqrtf(acc);
+    if (acc > 0.f && rank < max_rank) {
+      float inv;
+      pivot_root(acc, l33, inv);
+    }
   }
   L[0] = l00; L[1] = l10; L[2] = l11; L[3] = l20; L[4] = l21;
   L[5] = l22; L[6] = l30; L[7] = l31; L[8] = l32; L[9] = l33;
@@ -509,19 +521,19 @@ __global__ void __launch_bounds__(kBlockThreads, BSS_MIN_BLOCKS) bss_rollout_ker
       for (int i = 0; i < 10; ++i) mo[8 + i] = C[i];
     }
     // ok = finite(mean) & finite(cov) & 1 - kappa(s_bar) e_bar > 0 (belief.py:376-379)
-    bool fin = true;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) fin &= isfinite(mu[i]);
-#pragma unroll
-    for (int i = 0; i < 10; ++i) fin &= isfinite(C[i]);
+    const bool fin = all_finite8(mu) && all_finite8(C) && all_finite2(C[8], C[9]);
     const float kap = curvature(P.tr, mu[7]);
     const bool ok = fin && (1.f - kap * mu[6] > 0.f);
     dead |= !ok;
     // _finite_or_zero (controllers.py:231-235, 311-312)
 #pragma unroll
-    for (int i = 0; i < 8; ++i) mean[i] = isfinite(mu[i]) ? mu[i] : 0.f;
+    for (int i = 0; i < 8; ++i) mean[i] = mu[i];
+    if (__builtin_expect(!fin, 0)) {
 #pragma unroll
-    for (int i = 0; i < 10; ++i) C[i] = isfinite(C[i]) ? C[i] : 0.f;
+      for (int i = 0; i < 8; ++i) mean[i] = isfinite(mu[i]) ? mu[i] : 0.f;
+#pragma unroll
+      for (int i = 0; i < 10; ++i) C[i] = isfinite(C[i]) ? C[i] : 0.f;
+    }
     h_prev = h_cur;
     h_cur = dcbf(mean[6], sqrtf(fmaxf(C[9], 0.f)), P);
     if (P.n_obs) {

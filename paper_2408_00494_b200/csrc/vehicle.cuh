@@ -40,6 +40,7 @@ struct VehDev {
   float2 lf_nlr;   // (lf, -lr)
   float2 By_s;     // (Byf, -Byr): B alpha with alpha_r = -atan2(.) folded in
   float2 Cy, Dy;   // (Cyf, Cyr), (Dyf, Dyr)
+  float2 Bx, Cx;   // (Bxf, Bxr), (Cxf, Cxr): longitudinal pair of step_shared
 };
 
 // node[j] = {s_j, kappa_j, slope_j, s_{j+1}} plus a sentinel node[n].
@@ -137,6 +138,10 @@ __device__ __forceinline__ bool all_finite8(const float x[8]) {
   return m < __int_as_float(0x7f800000);
 }
 
+__device__ __forceinline__ bool all_finite2(float a, float b) {
+  return max2_nan(fabsf(a), fabsf(b)) < __int_as_float(0x7f800000);
+}
+
 // The step split in two: everything that depends only on (vx, omega_f,
 // omega_r, s) and the control -- the longitudinal slips and tire forces,
 // the wheel accelerations and kappa(s) -- is `step_shared`; the rest, which
@@ -172,7 +177,12 @@ __device__ __forceinline__ StepShared step_shared(const float x[8], const CtlDev
 #endif
   const float sgf = (wf * V.R - vx) * h.inv_den;
   const float sgr = (wr * V.R - vx) * h.inv_den;
+#ifdef BSS_EXACT_MATH
   const float txf = V.Cxf * atanf(V.Bxf * sgf), txr = V.Cxr * atanf(V.Bxr * sgr);
+#else
+  const float2 tx = __fmul2_rn(V.Cx, atan_x2(__fmul2_rn(V.Bx, make_float2(sgf, sgr))));
+  const float txf = tx.x, txr = tx.y;
+#endif
   float sxf, sxr;
 #if defined(BSS_EXACT_MATH)
   sincosf(txf, &sxf, &h.cx.x);
