@@ -129,8 +129,11 @@ __device__ __forceinline__ void belief_normals(const PhiloxKeys &rk, uint32_t t,
 // Config-4 extension: 4 re-projection normals + Laplace(0, b) on (vx, vy, r)
 // + U(-a, a) lateral slip on vy from the same two Philox4x32-7 blocks (the
 // second block's words become the uniforms instead of Box-Muller normals).
-__device__ __forceinline__ float centred_uniform(uint32_t w) {   // (-0.5, 0.5)
-  return ((float)(w >> 9) + 0.5f) * 1.1920928955078125e-07f - 0.5f;
+// 2u for the centred uniform u = (n + 1/2) 2^-23 - 1/2 of the top 23 bits n
+// of w, i.e. (2n + 1 - 2^23) 2^-23 in (-1, 1): the mantissa m = 1 + n 2^-23
+// by bit insertion, 2m - 3 (exact FFMA), + 2^-23 (exact) -- no I2F.
+__device__ __forceinline__ float centred_uniform2(uint32_t w) {
+  return fmaf(__uint_as_float(0x3f800000u | (w >> 9)), 2.0f, -3.0f) + 1.1920928955078125e-07f;
 }
 
 __device__ __forceinline__ void laplace_from_bits(const Philox4 &p, const Philox4 &q, float b, float a,
@@ -140,11 +143,11 @@ __device__ __forceinline__ void laplace_from_bits(const Philox4 &p, const Philox
   const uint32_t words[3] = {q.x, q.y, q.z};
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    const float u = centred_uniform(words[i]);
+    const float v = centred_uniform2(words[i]);   // 2u
     // inverse CDF: -b sgn(u) ln(1 - 2|u|)
-    w[i] = -b * copysignf(0.69314718056f * lg2_approx(1.0f - 2.0f * fabsf(u)), u);
+    w[i] = -b * copysignf(0.69314718056f * lg2_approx(1.0f - fabsf(v)), v);
   }
-  w[1] += 2.0f * a * centred_uniform(q.w);
+  w[1] += a * centred_uniform2(q.w);             // U(-a, a) = 2a u
 }
 
 // The 2 standard normals of control sample (k, t) (controllers.py:175).

@@ -5,12 +5,16 @@
 // sample build / moments, constraints.py:130-186 DCBF + shield penalty,
 // controllers.py:166-177 + 215-228 sampling and costs) as ONE kernel:
 //
-//   * one group of G lanes (G = min(32, pow2 >= M)) owns one rollout k and
-//     its M Monte-Carlo particles (lane l handles m = l, l+G, ...); with
-//     M >= 32 a warp is one rollout and no block-level sync exists at all;
-//   * particles never touch memory: re-projection x = mu + L z, the Euler
-//     step, process noise and the moment sums all stay in registers;
-//   * per-step moments use a shift c = step(mu_t) (the noise-free particle),
+//   * one group of G lanes owns one rollout k and its M Monte-Carlo
+//     particles (lane l handles m = l, l+G, ...); G is the power of two >= M
+//     (<= 32) narrowed by the measured policy in bssmppi.cu group_width
+//     (C3: G = 8, 4 rollouts per warp, 32 particles per lane); no
+//     block-level sync exists at all;
+//   * particles never touch memory: noise, re-projection x = mu + L z, the
+//     Euler step, process noise and the moment sums all stay in registers;
+//     the noise of particle m + G is generated inside particle m's
+//     iteration (software pipelining, particle_pass);
+//   * per-step moments use particle 0 of the group as the shift c,
 //     accumulating S1 = sum(x - c), S2 = sum((x - c)(x - c)^T) in ONE pass,
 //     reduced across the group with a reduce-scatter shuffle butterfly and
 //     all-gathered through 20 floats of shared memory; mean = c + S1/M,
@@ -18,9 +22,10 @@
 //     two-pass estimator; deviations from the shift are O(sigma) so FP32
 //     keeps tree-sum accuracy, and a zero-spread cloud collapses onto the
 //     deterministic step exactly (belief.py:282-284 guarantee);
-//   * everything per (k, t) -- control sample, clamp, control cost, stage
-//     cost, Cholesky, DCBF, penalty, frame check -- is computed
-//     redundantly by the G lanes (same issue slots as one lane).
+//   * everything per (k, t) -- stage cost, shared step terms, Cholesky,
+//     DCBF, penalty, frame check -- is computed redundantly by the G lanes
+//     (same issue slots as one lane); the controls, their clamp and the
+//     control cost are sampled once per (k, t) in the prologue.
 #pragma once
 #include <cstdint>
 
@@ -104,21 +109,30 @@ __device__ __forceinline__ float obstacle_terms(const RollParams &P, float s, fl
   const float f = fi - (float)j;
   const float4 a = P.cl[j], b = P.cl[j + 1];
   const float cx = fmaf(f, b.x - a.x, a.x), cy = fmaf(f, b.y - a.y, a.y), th = fmaf(f, b.z - a.z, a.z);
-  float st, ct;
-  sincosf(th, &st, &ct);
-  const float nx = -st, ny = ct;
+  const float2 sc = sincos_pi_x2(th);          // (sin, cos) of the centerline heading
+  const float nx = -sc.x, ny = sc.y;
   const float px = fmaf(ey, nx, cx), py = fmaf(ey, ny, cy);
   float h = __int_as_float(0x7f800000);
   inside = false;
   for (int i = 0; i < P.n_obs; ++i) {
     const float4 o = P.obs[i];
     const float dx = px - o.x, dy = py - o.y;
-    const float d = sqrtf(dx * dx + dy * dy);
+    const float d2 = dx * dx + dy * dy;
+    float inv;                                   // 1/d from one MUFU.RSQ (non-ftz approx)
+    asm("rsqrt.approx.f32 %0, %1;" : "=f"(inv) : "f"(d2));
+    const float d = d2 > 0.f ? d2 * inv : 0.f;
     inside |= d < o.z;
-    const float eta = (d > 0.f) ? (dx * nx + dy * ny) / d : 1.f;
+    const float eta = d2 > 0.f ? (dx * nx + dy * ny) * inv : 1.f;
     h = fminf(h, d - o.z - P.nu_obs * fabsf(eta) * sigy);
   }
   return h;
+}
+
+// sqrt(max(v, 0)) for sigma_y from one MUFU (non-ftz approx, ~2^-22 relative).
+__device__ __forceinline__ float sigma_of(float v) {
+  float r;
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(fmaxf(v, 0.f)));
+  return r;
 }
 
 // Per-(k,t) control: sample/clamp/control-cost (controllers.py:166-177, 223-228).
@@ -467,10 +481,10 @@ __global__ void __launch_bounds__(kBlockThreads, BSS_MIN_BLOCKS) bss_rollout_ker
     for (int i = 0; i < 10; ++i) C[i] = P.cov0[ui[i]];
   }
   chol4(C, L, 4);   // the initial belief covariance is not a sample estimate
-  float h_cur = dcbf(mean[6], sqrtf(fmaxf(C[9], 0.f)), P);
+  float h_cur = dcbf(mean[6], sigma_of(C[9]), P);
   float h_prev = h_cur;
   bool inside = false;
-  float ho_cur = P.n_obs ? obstacle_terms(P, mean[7], mean[6], sqrtf(fmaxf(C[9], 0.f)), inside) : 0.f;
+  float ho_cur = P.n_obs ? obstacle_terms(P, mean[7], mean[6], sigma_of(C[9]), inside) : 0.f;
   float ho_prev = ho_cur;
   bool dead = false;
   const float4 *ctl_row = P.ctl + (size_t)k * P.T;
@@ -535,10 +549,10 @@ __global__ void __launch_bounds__(kBlockThreads, BSS_MIN_BLOCKS) bss_rollout_ker
       for (int i = 0; i < 10; ++i) C[i] = isfinite(C[i]) ? C[i] : 0.f;
     }
     h_prev = h_cur;
-    h_cur = dcbf(mean[6], sqrtf(fmaxf(C[9], 0.f)), P);
+    h_cur = dcbf(mean[6], sigma_of(C[9]), P);
     if (P.n_obs) {
       ho_prev = ho_cur;
-      ho_cur = obstacle_terms(P, mean[7], mean[6], sqrtf(fmaxf(C[9], 0.f)), inside);
+      ho_cur = obstacle_terms(P, mean[7], mean[6], sigma_of(C[9]), inside);
     }
     if (!PERSIST) chol4(C, L, P.chol_rank);
   }
