@@ -107,3 +107,20 @@ def test_sincos_pi_x2_table_is_the_scalar_polynomials():
     assert sin_c[0] == 0.0
     assert sin_c[1:] == _coeffs("void sincos_pi")
     assert cos_c == _coeffs("void sincos_pi", "q")
+
+
+def test_centred_uniform2_is_exact():
+    """philox.cuh centred_uniform2: the I2F-free 2u (mantissa bit insertion,
+    FFMA 2m - 3, + 2^-23) equals 2 x the reference-form centred uniform
+    (n + 1/2) 2^-23 - 1/2 for every 23-bit n, and the derived Laplace
+    inputs 1 - |2u| and a (2u) are bit-identical to 1 - 2|u| and (2a) u."""
+    n = np.arange(0, 1 << 23, dtype=np.uint32)
+    m = (np.uint32(0x3F800000) | n).view(np.float32)
+    v = (m.astype(np.float64) * 2.0 - 3.0).astype(np.float32) + np.float32(2.0 ** -23)
+    assert np.array_equal((m.astype(np.float64) * 2.0 - 3.0), (m.astype(np.float64) * 2.0 - 3.0).astype(np.float32))
+    u = (n.astype(np.float32) + np.float32(0.5)) * np.float32(2.0 ** -23) - np.float32(0.5)
+    assert np.array_equal(v.astype(np.float64), 2.0 * u.astype(np.float64))
+    assert np.abs(v).max() < 1.0
+    assert np.array_equal(np.float32(1.0) - np.abs(v), np.float32(1.0) - np.float32(2.0) * np.abs(u))
+    a = np.float32(0.05)
+    assert np.array_equal(a * v, (np.float32(2.0) * a) * u)
