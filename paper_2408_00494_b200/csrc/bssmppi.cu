@@ -97,6 +97,9 @@ int validate(const bssmppi_problem *p) {
   if (p->kind < 0 || p->kind > 2) return fail(BSSMPPI_ERR_INVALID, "unknown controller kind %d", p->kind);
   if (p->samples < 1 || p->horizon < 1) return fail(BSSMPPI_ERR_INVALID, "samples and horizon must be >= 1");
   if (p->horizon > 512) return fail(BSSMPPI_ERR_UNSUPPORTED, "horizon %d > 512", p->horizon);
+  if (!(p->phys[7] > 0.0 && p->phys[7] <= 2.0 && p->phys[9] > 0.0 && p->phys[9] <= 2.0))
+    return fail(BSSMPPI_ERR_UNSUPPORTED, "lateral magic-formula shape factors C must lie in (0, 2] "
+                "(got %g, %g): the device tire sine covers |C atan(.)| <= pi", p->phys[7], p->phys[9]);
   if (!(p->temperature > 0.0)) return fail(BSSMPPI_ERR_INVALID, "temperature must be > 0");
   if (p->kind == BSSMPPI_KIND_BSS && p->inner_samples < 2)
     return fail(BSSMPPI_ERR_INVALID, "bss controller needs inner_samples >= 2");
@@ -206,7 +209,6 @@ void fill_params(bssmppi_ctx *c, const bssmppi_problem *p) {
   V.drive = (float)q[18]; V.vfloor = (float)q[20];
   V.rrf = (float)(q[19] * q[21] * q[4]); V.rrr = (float)(q[19] * q[22] * q[4]);
   V.spin_scale = (float)(q[4] / 0.1); V.dt = (float)p->dt;
-  V.mf_poly = (std::max(std::max(q[7], q[9]), std::max(q[11], q[13])) <= 1.3) ? 1 : 0;
   V.lf_nlr = make_float2(V.lf, -V.lr);
   V.By_s = make_float2(V.Byf, -V.Byr);
   V.Cy = make_float2(V.Cyf, V.Cyr);

@@ -10,33 +10,6 @@
 
 namespace bss {
 
-// sin(x), |x| <= 2.05: the magic-formula angle C*atan(.) for C <= 1.3.
-__device__ __forceinline__ float sin_mf(float x) {
-  const float t = x * x;
-  float p = 1.486371581e-10f;
-  p = fmaf(p, t, -2.497564111e-08f);
-  p = fmaf(p, t, 2.755482001e-06f);
-  p = fmaf(p, t, -1.984122646e-04f);
-  p = fmaf(p, t, 8.333332837e-03f);
-  p = fmaf(p, t, -1.666666716e-01f);
-  p = fmaf(p, t, 1.0f);
-  return p * x;
-}
-
-// cos(x), |x| <= 2.05.
-__device__ __forceinline__ float cos_mf(float x) {
-  const float t = x * x;
-  float p = -1.069323536e-11f;
-  p = fmaf(p, t, 2.082424899e-09f);
-  p = fmaf(p, t, -2.755546120e-07f);
-  p = fmaf(p, t, 2.480155126e-05f);
-  p = fmaf(p, t, -1.388888806e-03f);
-  p = fmaf(p, t, 4.166666791e-02f);
-  p = fmaf(p, t, -5.0e-01f);
-  p = fmaf(p, t, 1.0f);
-  return p;
-}
-
 // sin and cos on any x: reduced to [-pi, pi] (a no-op for heading errors,
 // which the step keeps in (-pi, pi]).
 __device__ __forceinline__ void sincos_pi(float x, float &s, float &c) {
@@ -106,6 +79,20 @@ __constant__ float2 kSinCosPi[9] = {
     {2.755584774e-06f, 2.480155672e-05f}, {-1.984121918e-04f, -1.388888806e-03f},
     {8.333332837e-03f, 4.166666791e-02f}, {-1.666666716e-01f, -5.0e-01f},
     {1.0f, 1.0f}};
+
+// sin of two arguments in [-pi, pi] (the sincos_pi sine polynomial, packed;
+// ~1 ulp, relative accuracy kept near 0 unlike MUFU.SIN's absolute 2^-21.4).
+__device__ __forceinline__ float2 sin_pi_x2(float2 x) {
+  const float2 t = __fmul2_rn(x, x);
+  float2 p = __ffma2_rn(t, bc2(-6.416872784e-13f), bc2(1.582333015e-10f));
+  p = __ffma2_rn(p, t, bc2(-2.502759777e-08f));
+  p = __ffma2_rn(p, t, bc2(2.755584774e-06f));
+  p = __ffma2_rn(p, t, bc2(-1.984121918e-04f));
+  p = __ffma2_rn(p, t, bc2(8.333332837e-03f));
+  p = __ffma2_rn(p, t, bc2(-1.666666716e-01f));
+  p = __ffma2_rn(p, t, bc2(1.0f));
+  return __fmul2_rn(p, x);
+}
 
 // returns (sin x, cos x), any x (reduced to [-pi, pi] as in sincos_pi)
 __device__ __forceinline__ float2 sincos_pi_x2(float x) {

@@ -35,7 +35,6 @@ struct VehDev {
   float Byf, Cyf, Byr, Cyr, Bxf, Cxf, Bxr, Cxr;
   float Dxf, Dyf, Dxr, Dyr;
   float drive, vfloor, rrf, rrr, spin_scale, dt;
-  int mf_poly;   // all magic-formula C <= 1.3: angles fit sin_mf/cos_mf's range
   // front/rear lane pairs of the packed (FFMA2) particle step
   float2 lf_nlr;   // (lf, -lr)
   float2 By_s;     // (Byf, -Byr): B alpha with alpha_r = -atan2(.) folded in
@@ -187,19 +186,15 @@ __device__ __forceinline__ StepShared step_shared(const float x[8], const CtlDev
 #if defined(BSS_EXACT_MATH)
   sincosf(txf, &sxf, &h.cx.x);
   sincosf(txr, &sxr, &h.cx.y);
-#elif defined(BSS_POLY_TIRE)
-  if (V.mf_poly) {
-    sxf = sin_mf(txf); h.cx.x = cos_mf(txf);
-    sxr = sin_mf(txr); h.cx.y = cos_mf(txr);
-  } else {
-    sincosf(txf, &sxf, &h.cx.x);
-    sincosf(txr, &sxr, &h.cx.y);
-  }
 #else
-  // MUFU sin/cos (|error| ~3.6e-7 on |theta| <= 2.05): same parity as the
-  // polynomial in the harness at less cost
-  __sincosf(txf, &sxf, &h.cx.x);
-  __sincosf(txr, &sxr, &h.cx.y);
+  // polynomial sin/cos (relative accuracy near 0; MUFU.SIN's absolute
+  // 2^-21.4 error is a large relative force error at small slips and drifts
+  // the deterministic belief mean by ~1e-4 over a horizon)
+  {
+    const float2 sf = sincos_pi_x2(txf), sr = sincos_pi_x2(txr);
+    sxf = sf.x; h.cx.x = sf.y;
+    sxr = sr.x; h.cx.y = sr.y;
+  }
 #endif
   h.cx.x = fabsf(h.cx.x);
   h.cx.y = fabsf(h.cx.y);
@@ -282,7 +277,8 @@ __device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, c
   }
   // (B_f alpha_f, B_r alpha_r), alpha_f = delta - A.x, alpha_r = -A.y
   const float2 ty = __fmul2_rn(V.Cy, atan_x2(__fmul2_rn(V.By_s, make_float2(c.delta - A.x, A.y))));
-  const float2 fy = __fmul2_rn(__fmul2_rn(V.Dy, make_float2(__sinf(ty.x), __sinf(ty.y))), h.cx);
+  // |ty| < C pi / 2 <= pi (lateral C <= 2, checked at context creation)
+  const float2 fy = __fmul2_rn(__fmul2_rn(V.Dy, sin_pi_x2(ty)), h.cx);
   // body-frame front force + rear longitudinal: (fxf cd - fyf sd + fxr, fxf sd + fyf cd)
   const float2 fb = __ffma2_rn(bc2(fy.x), h.nsd_cd, h.fb0);
   // (dvx, dvy) = (fb.x, fb.y + fyr) / m + (vy r, -vx r)

@@ -71,6 +71,29 @@ def test_validation_before_cuda():
     assert b"samples" in lib.bssmppi_last_error()
 
 
+def test_lateral_shape_factor_range_checked_before_cuda():
+    """The device tire sine covers |C atan(.)| <= pi: a lateral magic-formula
+    shape factor above 2 is refused at context creation (before any CUDA
+    call) instead of returning wrong forces."""
+    from dataclasses import replace
+    from helpers import Inputs
+    from paper_2408_00494_b200 import controllers as mc
+
+    inp = Inputs("c1_s0")
+    lib = _lib.load()
+    h = ctypes.c_void_p()
+    for cyf, expect in ((2.5, _lib.ERR_UNSUPPORTED), (2.0, None)):
+        model = replace(inp.model, c_lat_front=cyf)
+        ctx = mc.RolloutContext(model, inp.track, inp.cost, noise=inp.noise)
+        prob, _keep = mc.build_problem("bss", 64, 10, 16, 1.0, 0.1, inp.cfg.sigma_eps, inp.cfg.precision,
+                                       inp.cfg.bounds, False, ctx)
+        rc = lib.bssmppi_create(ctypes.byref(prob), 0, ctypes.byref(h))
+        if expect is None:
+            assert rc != _lib.ERR_UNSUPPORTED      # passes validation (then needs a GPU)
+        else:
+            assert rc == expect and b"shape factors" in lib.bssmppi_last_error()
+
+
 def test_no_cpu_fallback_without_gpu():
     import torch
     if torch.cuda.is_available():

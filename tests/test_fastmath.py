@@ -42,16 +42,6 @@ def _check(c, x, exact, odd, abs_tol, rel_tol=None):
         assert (e[big] / ex[big]).max() < rel_tol
 
 
-def test_sin_mf():
-    x = np.linspace(-2.05, 2.05, 200001)
-    _check(_coeffs("float sin_mf"), x, np.sin, True, 3e-7, 5e-7)
-
-
-def test_cos_mf():
-    x = np.linspace(-2.05, 2.05, 200001)
-    _check(_coeffs("float cos_mf"), x, np.cos, False, 3e-7)
-
-
 def test_sincos_pi():
     x = np.linspace(-np.pi, np.pi, 200001)
     _check(_coeffs("void sincos_pi"), x, np.sin, True, 5e-7)
@@ -61,9 +51,16 @@ def test_sincos_pi():
     _check(_coeffs("void sincos_pi"), xs, np.sin, True, 1e-7, 3e-7)
 
 
-def test_magic_formula_angle_bound():
-    # C * atan(.) stays inside sin_mf's range for the default C = 1.3
-    assert 1.3 * np.pi / 2 < 2.05
+def test_sin_pi_x2_is_the_sincos_pi_sine():
+    """The packed tire sine (lateral C atan(.), |.| <= pi for C <= 2) runs the
+    sincos_pi sine polynomial: same coefficients, same Horner order."""
+    body = SRC[SRC.index("float2 sin_pi_x2"):]
+    body = body[:body.index("\n}\n")]
+    c = [np.float32(float(v)) for v in re.findall(r"bc2\(([-0-9.e+]+)f\)", body)]
+    assert c == _coeffs("void sincos_pi")
+    from paper_2408_00494_b200.dynamics import VehicleParams
+    p = VehicleParams()
+    assert 0 < p.c_lat_front <= 2.0 and 0 < p.c_lat_rear <= 2.0   # the default car is supported
 
 
 def _atan_x2_coeffs():
