@@ -108,3 +108,14 @@ def test_no_cpu_fallback_without_gpu():
     with pytest.raises(_lib.BssMppiError):
         mc.mppi_update(mc.RolloutBatch(np.zeros((2, 3, 2)), np.zeros((2, 3, 2)), np.ones(2)), 1.0,
                        mc.ControlBounds())
+
+
+def test_integration_binding_matches_the_abi():
+    """INTEGRATION.md's ctypes mirror of bssmppi_problem (what a maintainer
+    would paste into the reference package) lists exactly the header's
+    fields, in order."""
+    import re
+    from pathlib import Path
+    txt = (Path(__file__).resolve().parent.parent / "INTEGRATION.md").read_text()
+    seg = txt[txt.index("class Problem"):txt.index("assert lib.bssmppi_abi_version")]
+    assert re.findall(r'\("([a-z_0-9]+)", ', seg) == _struct_fields("bssmppi_problem")
