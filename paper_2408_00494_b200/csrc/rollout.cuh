@@ -426,7 +426,7 @@ __device__ __forceinline__ void accumulate(float acc[18], const float x[8], cons
 // Software-pipelined noise: the Philox blocks and Box-Muller transforms of
 // particle m + G are produced inside particle m's iteration, so the
 // quarter-rate IMAD.WIDE / MUFU work overlaps the FP32 dynamics in one
-// scheduling region (one extra noise draw per lane and step).
+// scheduling region; the last particle is peeled, so no draw is wasted.
 template <int G, bool PERSIST, bool ZARR, int NK>
 __device__ __forceinline__ void particle_pass(const RollParams &P, int t, int k, int kg, int li,
                                               const float mean[8], const float L[10], const CtlDev &ctl,
@@ -436,16 +436,21 @@ __device__ __forceinline__ void particle_pass(const RollParams &P, int t, int k,
   const bool has0 = li < M;
   float x[8], zc[7], zn[7];
   particle_noise<ZARR, NK>(P, t, k, kg, li, zc);
-  particle_noise<ZARR, NK>(P, t, k, kg, li + G, zn);
+  if (li + G < M) particle_noise<ZARR, NK>(P, t, k, kg, li + G, zn);
   if (has0) particle_step<PERSIST, NK>(P, t, li, mean, L, ctl, sh, cloud, zc, x);
 #pragma unroll
   for (int i = 0; i < 8; ++i) c[i] = __shfl_sync(0xffffffffu, x[i], 0, G);
   if (has0) accumulate<!PERSIST>(acc, x, c);
-  for (int m = li + G; m < M; m += G) {
+  int m = li + G;
+  for (; m + G < M; m += G) {             // steady state: look one particle ahead
 #pragma unroll
     for (int j = 0; j < 7; ++j) zc[j] = zn[j];
     particle_noise<ZARR, NK>(P, t, k, kg, m + G, zn);
     particle_step<PERSIST, NK>(P, t, m, mean, L, ctl, sh, cloud, zc, x);
+    accumulate<!PERSIST>(acc, x, c);
+  }
+  if (m < M) {                            // last particle: no look-ahead draw
+    particle_step<PERSIST, NK>(P, t, m, mean, L, ctl, sh, cloud, zn, x);
     accumulate<!PERSIST>(acc, x, c);
   }
 }
