@@ -163,12 +163,6 @@ __device__ __forceinline__ void control_at(const RollParams &P, int k, int kg, i
   ccost = P.gamma * (v0 * (P.prec[0] * a0 + P.prec[1] * a1) + v1 * (P.prec[2] * a0 + P.prec[3] * a1));
 }
 
-// 4x4 PSD Cholesky with zero-pivot columns left zero (belief.py:235-256).
-// A column is dropped when its pivot is not positive -- exact for the
-// structurally zero rows (noise-free components, zero initial covariance),
-// like the reference's 1e-300 clamp -- and, because a sample covariance of
-// M particles has rank <= M - 1, at most M - 1 pivots are kept (for M <= 4
-// the FP64 reference's extra pivots are rounding noise of O(1e-8 sigma)).
 // sqrt(p) and 1/sqrt(p) of a positive pivot from one MUFU.RSQ (the non-ftz
 // approx form keeps denormal pivots; relative error ~2^-22, far below the
 // FP32 sample-covariance noise) instead of IEEE sqrtf + division.
@@ -177,6 +171,12 @@ __device__ __forceinline__ void pivot_root(float p, float &l, float &inv) {
   l = p * inv;
 }
 
+// 4x4 PSD Cholesky with zero-pivot columns left zero (belief.py:235-256).
+// A column is dropped when its pivot is not positive -- exact for the
+// structurally zero rows (noise-free components, zero initial covariance),
+// like the reference's 1e-300 clamp -- and, because a sample covariance of
+// M particles has rank <= M - 1, at most M - 1 pivots are kept (for M <= 4
+// the FP64 reference's extra pivots are rounding noise of O(1e-8 sigma)).
 __device__ __forceinline__ void chol4(const float C[10], float L[10], int max_rank) {
   // packed lower: L00 L10 L11 L20 L21 L22 L30 L31 L32 L33
   // C packed upper: c00 c01 c02 c03 c11 c12 c13 c22 c23 c33
@@ -283,8 +283,10 @@ __device__ __forceinline__ void group_allreduce18(float a[18], int li, float *sl
 
 constexpr int kSlotFloats = 20;   // 18 sums, 16-byte aligned slot
 constexpr int kBlockThreads = 128;
-// Register budget: 5 resident 128-thread blocks per SM (<= 102 registers,
-// 20 warps/SM) measured fastest at C3 (96 vs 113 registers: -2%).
+// Register budget: 4 resident 128-thread blocks per SM (<= 128 registers,
+// 16 warps/SM).  With the software-pipelined noise (particle_pass) the extra
+// registers buy more than occupancy: 5 / 6 / 7 blocks per SM (96 / 80 / 72
+// registers) measured slower at C3 (profiles/README.md).
 #ifndef BSS_MIN_BLOCKS
 #define BSS_MIN_BLOCKS 4
 #endif
@@ -332,10 +334,9 @@ __device__ __forceinline__ float control_prologue(const RollParams &P, int k, in
 // normals scaled by F after the step (the column layout of the reference's
 // z_all block, controllers.py:285-287, belief.py:328-333) or, for the
 // config-4 extension, the Laplace + slip increments themselves.  ZARR reads
-// the reference's normals (zeros past M, where the pipelined loop looks
-// one particle ahead).
-// NK: noise kind (0 Gaussian, 1 Laplace + slip) as a template parameter, so
-// the pipelined loop body is one scheduling region.
+// the reference's normals (guarded to zeros for m >= M).  NK, the noise
+// kind (0 Gaussian, 1 Laplace + slip), is a template parameter so that the
+// pipelined loop body of particle_pass is one scheduling region.
 template <bool ZARR, int NK>
 __device__ __forceinline__ void particle_noise(const RollParams &P, int t, int k, int kg, int m, float n[7]) {
   if (ZARR) {
