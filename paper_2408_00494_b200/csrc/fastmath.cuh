@@ -3,7 +3,10 @@
 // The libdevice versions (sinf/sincosf/atan2f/division) carry range
 // reduction and IEEE slow paths the particle step never needs; these keep
 // ~1-3 ulp accuracy on the ranges that occur and cost a handful of FMAs.
-// Coefficients are Lawson-iterated least-squares fits (tools/fit_poly.py);
+// Coefficients are Lawson-iterated (minimax) least-squares fits: the atan
+// constants are `tools/fit_poly.py atan` output verbatim; the sin/cos ones
+// come from an earlier fit of the same kind (`tools/fit_poly.py sincos_pi`
+// reproduces them to within the pinned bounds, not bit for bit).
 // tests/test_fastmath.py re-evaluates every polynomial in float32 (same
 // Horner order) against float64 and pins the error bounds.
 #pragma once
