@@ -54,19 +54,19 @@ __device__ __forceinline__ float rcp_approx(float x) {
 }
 
 // atan of two arguments: a = min(|x|, 1/|x|) in [0, 1], atan(a) = a + a s P(s)
-// with s = a^2 (degree-7 minimax in s, tools/fit_poly.py atan: 1.9 ulp on
-// the whole line), pi/2 - atan(a) for |x| > 1, sign of x.  inf -> +-pi/2.
+// with s = a^2 (degree-6 minimax in s, tools/fit_poly.py atan: 3.0 ulp /
+// 1.8e-7 absolute on the whole line; degree 7 was 1.9 ulp at 1.2% more
+// time and the same parity), pi/2 - atan(a) for |x| > 1, sign of x.
 __device__ __forceinline__ float2 atan_x2(float2 x) {
   const float tx = fabsf(x.x), ty = fabsf(x.y);
   const float2 a = make_float2(fminf(tx, rcp_approx(tx)), fminf(ty, rcp_approx(ty)));
   const float2 s = __fmul2_rn(a, a);
-  float2 p = __ffma2_rn(s, bc2(2.920688828e-03f), bc2(-1.636791416e-02f));
-  p = __ffma2_rn(p, s, bc2(4.321184009e-02f));
-  p = __ffma2_rn(p, s, bc2(-7.552212477e-02f));
-  p = __ffma2_rn(p, s, bc2(1.066600382e-01f));
-  p = __ffma2_rn(p, s, bc2(-1.421105564e-01f));
-  p = __ffma2_rn(p, s, bc2(1.999377310e-01f));
-  p = __ffma2_rn(p, s, bc2(-3.333315253e-01f));
+  float2 p = __ffma2_rn(s, bc2(-4.822528455e-03f), bc2(2.473404258e-02f));
+  p = __ffma2_rn(p, s, bc2(-6.020310149e-02f));
+  p = __ffma2_rn(p, s, bc2(9.968471527e-02f));
+  p = __ffma2_rn(p, s, bc2(-1.404132694e-01f));
+  p = __ffma2_rn(p, s, bc2(1.997421384e-01f));
+  p = __ffma2_rn(p, s, bc2(-3.333239257e-01f));
   p = __fmul2_rn(p, s);
   p = __ffma2_rn(a, p, a);
   const float2 q = __fadd2_rn(bc2(1.57079637f), make_float2(-p.x, -p.y));

@@ -67,27 +67,27 @@ def _atan_x2_coeffs():
     body = SRC[SRC.index("float2 atan_x2"):]
     body = body[:body.index("\n}\n")]
     first = re.findall(r"bc2\(([-0-9.e+]+)f\)", body)
-    return [np.float32(float(v)) for v in first[:8]]
+    return [np.float32(float(v)) for v in first[:7]]
 
 
 def test_atan_x2():
-    """Packed arctangent (slip angles and lateral magic formula): the
-    device algorithm in float32 with the kernel's Horner order, <= 2 ulp /
-    1.7e-7 absolute on the whole line (libdevice atanf is specified at 2 ulp)."""
+    """Packed arctangent (slip angles and both magic formulas): the device
+    algorithm in float32 with the kernel's Horner order, <= 3.1 ulp /
+    1.85e-7 absolute on the whole line (libdevice atanf: 2 ulp)."""
     import sys
     sys.path.insert(0, str(Path(__file__).resolve().parent.parent / "tools"))
     from fit_poly import atan32
     c = np.array(_atan_x2_coeffs(), dtype=np.float64)
-    assert len(c) == 8
+    assert len(c) == 7
     x = np.concatenate([np.linspace(-40, 40, 400001), np.geomspace(1e-6, 1e6, 100001),
                         -np.geomspace(1e-6, 1e6, 1001), [0.0, np.inf, -np.inf]])
     x = x.astype(np.float32).astype(np.float64)
     y = atan32(c, x)
     ex = np.arctan(x)
     e = np.abs(y - ex)
-    assert e.max() < 1.7e-7, e.max()
+    assert e.max() < 1.85e-7, e.max()
     ulp = np.spacing(np.abs(ex).astype(np.float32)).astype(np.float64)
-    assert (e / ulp).max() <= 2.0
+    assert (e / ulp).max() <= 3.1
     assert np.all(np.sign(y) == np.sign(x))
 
 
