@@ -54,9 +54,10 @@ typedef struct bssmppi_problem {
   /* MppiConfig (controllers.py:71-105) */
   int32_t kind;                 /* BSSMPPI_KIND_* */
   int32_t samples;              /* K (global, all shards) */
-  int32_t horizon;              /* T */
-  int32_t inner_samples;        /* M (bss only; >= 2) */
-  int32_t persist_particles;    /* controllers.py:83 */
+  int32_t horizon;              /* T (<= 512) */
+  int32_t inner_samples;        /* M (bss only; 2..8192) */
+  int32_t persist_particles;    /* controllers.py:83; the cloud lives in shared
+                                   memory, so M <= 1792 (else UNSUPPORTED) */
   double temperature;           /* lambda */
   double control_cost_weight;   /* gamma */
   double sigma_factor[4];       /* psd_factor(sigma_eps), 2x2 row-major */

@@ -92,6 +92,9 @@ struct DeviceGuard {
   }
 };
 
+constexpr size_t kSmemMax = 227 * 1024;   // opt-in dynamic shared memory per block
+constexpr int kPersistMaxM = 1792;         // persist clouds of one G = 32 block fit kSmemMax
+
 int validate(const bssmppi_problem *p) {
   if (!p) return fail(BSSMPPI_ERR_INVALID, "problem is NULL");
   if (p->kind < 0 || p->kind > 2) return fail(BSSMPPI_ERR_INVALID, "unknown controller kind %d", p->kind);
@@ -105,6 +108,9 @@ int validate(const bssmppi_problem *p) {
     return fail(BSSMPPI_ERR_INVALID, "bss controller needs inner_samples >= 2");
   if (p->kind == BSSMPPI_KIND_BSS && p->inner_samples > 8192)
     return fail(BSSMPPI_ERR_UNSUPPORTED, "inner_samples %d > 8192", p->inner_samples);
+  if (p->kind == BSSMPPI_KIND_BSS && p->persist_particles && p->inner_samples > kPersistMaxM)
+    return fail(BSSMPPI_ERR_UNSUPPORTED, "persist_particles keeps the cloud in shared memory: inner_samples %d > %d",
+                p->inner_samples, kPersistMaxM);
   if (p->k_count < 1 || p->k_begin < 0 || (int64_t)p->k_begin + p->k_count > p->samples)
     return fail(BSSMPPI_ERR_INVALID, "shard [%d, %d) outside K=%d", p->k_begin, p->k_begin + p->k_count, p->samples);
   if (!p->track_s || !p->track_kappa || p->track_n < 2)
@@ -262,6 +268,19 @@ int group_width(int M, int K) {
   return g;
 }
 
+// Persist mode keeps each rollout's cloud ([8][M] floats) in shared memory:
+// widen the group until a block's clouds fit (G = 32 holds M <= kPersistMaxM).
+size_t persist_smem(int g, int M) {
+  return (size_t)(kBlockThreads / 32) * (32 / g) * 2 * kSlotFloats * sizeof(float) +
+         (size_t)(kBlockThreads / g) * 8 * M * sizeof(float);
+}
+
+int rollout_group_width(int M, int K, bool persist) {
+  int g = group_width(M, K);
+  while (persist && g < 32 && persist_smem(g, M) > kSmemMax) g <<= 1;
+  return g;
+}
+
 template <int G>
 cudaError_t launch_bss_g(const RollParams &rp, bool persist, bool zarr, cudaStream_t st) {
   constexpr int GPB = kBlockThreads / G;   // rollouts per block
@@ -282,7 +301,7 @@ cudaError_t launch_bss_g(const RollParams &rp, bool persist, bool zarr, cudaStre
 int launch_rollout(bssmppi_ctx *c, const RollParams &rp, bool zarr) {
   cudaError_t e;
   if (c->kind == BSSMPPI_KIND_BSS) {
-    switch (group_width(rp.M, rp.k_count)) {
+    switch (rollout_group_width(rp.M, rp.k_count, c->persist != 0)) {
       case 2: e = launch_bss_g<2>(rp, c->persist, zarr, c->stream); break;
       case 4: e = launch_bss_g<4>(rp, c->persist, zarr, c->stream); break;
       case 8: e = launch_bss_g<8>(rp, c->persist, zarr, c->stream); break;
