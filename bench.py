@@ -34,8 +34,20 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-FLOP_PER_PARTICLE_STEP = 162      # SURVEY.md 8d algorithmic FP32 FLOP (FMA = 2)
-SFU_PER_PARTICLE_STEP = 16         # SURVEY.md 8d algorithmic transcendental evaluations
+# algorithmic work of one particle-step, counted from the
+# reference formulation (FMA = 2 FLOP, add/sub/mul/div = 1; transcendental
+# evaluations counted separately; per-(k,t) shared work excluded).
+# (block, reference lines, FP32 FLOP, transcendentals)
+WORK_TABLE = (
+    ("re-projection x = mu + L z (lower-triangular 4x4)", "belief.py:264-272", 20, 0),
+    ("process noise (diagonal F: 3 mul) + add to 3 channels", "belief.py:369, dynamics.py:571-572", 6, 0),
+    ("tires: 2 atan2, 4 atan, 4 sin, 2 sqrt", "dynamics.py:375-395", 31, 12),
+    ("derivatives + curvature: 2 tanh, sin + cos(e_psi)", "dynamics.py:409-437, 341-369", 49, 4),
+    ("Euler update + angle / arc-length wraps", "dynamics.py:479-489", 24, 0),
+    ("moments: mean 8 adds, cov 4 sub + 10 FMA", "belief.py:283-308", 32, 0),
+)
+FLOP_PER_PARTICLE_STEP = sum(r[2] for r in WORK_TABLE)   # 162
+SFU_PER_PARTICLE_STEP = sum(r[3] for r in WORK_TABLE)    # 16
 METRIC = "belief rollout-steps/s (K*M*T/s)"
 UNIT = "rollout-steps/s"
 

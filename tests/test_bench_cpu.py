@@ -49,3 +49,19 @@ def test_device_arm_fails_loudly_without_gpu():
     r = _bench("--steps", "1", "--warmup", "3", "--no-cpu-baseline")
     assert r.returncode != 0
     assert r.stdout.strip() == ""          # no JSON line, no CPU fallback number
+
+
+def test_algorithmic_work_table():
+    """SURVEY.md 8d's per-particle-step work, pinned row by row: the
+    roofline's `achieved` numbers are these counts x K M T / kernel time."""
+    sys.path.insert(0, str(ROOT))
+    import bench
+    rows = {r[0].split(":")[0].split(" (")[0]: (r[2], r[3]) for r in bench.WORK_TABLE}
+    assert bench.FLOP_PER_PARTICLE_STEP == 162 and bench.SFU_PER_PARTICLE_STEP == 16
+    # rows that follow from the algebra alone
+    assert rows["re-projection x = mu + L z"] == (2 * 10, 0)            # 10 multiply-adds of L (4x4 lower)
+    assert rows["process noise"] == (3 + 3, 0)                           # 3 mul + 3 add
+    assert rows["moments"] == (8 + 4 + 2 * 10, 0)                       # 8 adds, 4 sub, 10 FMA
+    assert rows["tires"][1] == 2 + 4 + 4 + 2                             # atan2, atan, sin, sqrt
+    assert rows["derivatives + curvature"][1] == 2 + 2                  # tanh x2, sin + cos
+    assert all(r[1] for r in bench.WORK_TABLE)                           # every row cites the reference
