@@ -324,7 +324,7 @@ int launch_update(bssmppi_ctx *c, bool final_, double *rec_out) {
   const int T2 = 2 * c->T;
   update_partials_kernel<float, float><<<c->nblocks, kUpdThreads, 0, c->stream>>>(
       c->k_count, c->k_begin, T2, c->d_cost, c->d_u, c->lam, c->chunk, c->d_rec);
-  combine_kernel<<<1, kUpdThreads, 0, c->stream>>>(
+  combine_kernel<<<1, kCombThreads, 0, c->stream>>>(
       c->nblocks, T2, c->d_rec, c->lam, final_ ? 1 : 0, rec_out, c->lo[0], c->lo[1], c->hi[0],
       c->hi[1], c->d_out, c->d_state + 24, c->d_out + T2);
   cudaError_t e = cudaGetLastError();
@@ -576,7 +576,7 @@ int bssmppi_enqueue_combine(bssmppi_ctx *c, const double *partials_dev, int32_t 
   if (!partials_dev || nslots < 1 || nslots > 1024) return fail(BSSMPPI_ERR_INVALID, "bad partials / nslots");
   DeviceGuard guard(c->device);
   const int T2 = 2 * c->T;
-  combine_kernel<<<1, kUpdThreads, 0, c->stream>>>(nslots, T2, partials_dev, c->lam, 1, nullptr, c->lo[0],
+  combine_kernel<<<1, kCombThreads, 0, c->stream>>>(nslots, T2, partials_dev, c->lam, 1, nullptr, c->lo[0],
                                                    c->lo[1], c->hi[0], c->hi[1], c->d_out, c->d_state + 24,
                                                    c->d_out + T2);
   CUDA_TRY(cudaGetLastError());
@@ -643,7 +643,7 @@ int bssmppi_mppi_update(int32_t K, int32_t T, const double *costs, const double 
     if (e == cudaSuccess) e = cudaMemcpy(d_u, controls, (size_t)K * T2 * sizeof(double), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) {
       update_partials_kernel<double, double><<<nblocks, kUpdThreads>>>(K, 0, T2, d_c, d_u, temperature, chunk, d_rec);
-      combine_kernel<<<1, kUpdThreads>>>(nblocks, T2, d_rec, temperature, 1, nullptr, lo[0], lo[1], hi[0], hi[1],
+      combine_kernel<<<1, kCombThreads>>>(nblocks, T2, d_rec, temperature, 1, nullptr, lo[0], lo[1], hi[0], hi[1],
                                          d_out, nullptr, d_out + T2);
       e = cudaGetLastError();
     }

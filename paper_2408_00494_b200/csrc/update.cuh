@@ -15,6 +15,7 @@ namespace bss {
 
 constexpr int kRecHead = 5;   // beta, Z, Z2, n_finite, argmin
 constexpr int kUpdThreads = 256;
+constexpr int kCombThreads = 512;     // combine_kernel: more loads in flight for the column pass
 constexpr int kCombineSlices = 16;    // record slices per column in combine_kernel
 constexpr int kCombinePart = 2048;    // slice partials held in shared memory (16 KB)
 
@@ -78,10 +79,10 @@ update_partials_kernel(int n, int k_begin, int T2, const CT *costs, const UT *u,
     for (int j = 0; j < 4; ++j) {
       const int col = tid + j * kUpdThreads;
       if (col < T2) {
-        // 8 loads in flight per thread (each is an L2 round trip)
+        // 16 loads in flight per thread (each is an L2 round trip)
         double a = nacc[j];
         const UT *up = u + (size_t)base * T2 + col;
-#pragma unroll 8
+#pragma unroll 16
         for (int i = 0; i < cnt_k; ++i) a = fma(s_w[i], to_d(up[(size_t)i * T2]), a);
         nacc[j] = a;
       }
@@ -113,14 +114,14 @@ update_partials_kernel(int n, int k_begin, int T2, const CT *costs, const UT *u,
 // v+ = clip(N/Z) -> vplus (double), warm-start shifted plan
 // (ControlPlan.shifted, controllers.py:154-156) -> plan_out (float, may be
 // null), head {beta, Z, Z2, n, argmin} -> head_out.
-__global__ void __launch_bounds__(kUpdThreads)
+__global__ void __launch_bounds__(kCombThreads)
 combine_kernel(int nrec, int T2, const double *rec, double lam, int final_, double *rec_out,
                double lo0, double lo1, double hi0, double hi1, double *vplus, float *plan_out,
                double *head_out) {
   __shared__ double s_scale[1024];
   __shared__ double s_part[kCombinePart];
-  __shared__ double s_a[kUpdThreads], s_b[kUpdThreads], s_c[kUpdThreads];
-  __shared__ long long s_i[kUpdThreads];
+  __shared__ double s_a[kCombThreads], s_b[kCombThreads], s_c[kCombThreads];
+  __shared__ long long s_i[kCombThreads];
   __shared__ double s_head[kRecHead];
   const int tid = threadIdx.x;
   const int R = kRecHead + T2;
@@ -128,7 +129,7 @@ combine_kernel(int nrec, int T2, const double *rec, double lam, int final_, doub
   // 1. global minimum (ties -> smallest k) and finite count
   double mn = INF, cnt = 0.0;
   long long arg = -1;
-  for (int r = tid; r < nrec; r += kUpdThreads) {
+  for (int r = tid; r < nrec; r += kCombThreads) {
     const double *h = rec + (size_t)r * R;
     if (h[3] > 0.0) {
       cnt += h[3];
@@ -138,7 +139,7 @@ combine_kernel(int nrec, int T2, const double *rec, double lam, int final_, doub
   }
   s_a[tid] = mn; s_i[tid] = arg; s_c[tid] = cnt;
   __syncthreads();
-  for (int s = kUpdThreads / 2; s > 0; s >>= 1) {
+  for (int s = kCombThreads / 2; s > 0; s >>= 1) {
     if (tid < s) {
       const double a = s_a[tid], b = s_a[tid + s];
       const long long ia = s_i[tid], ib = s_i[tid + s];
@@ -153,7 +154,7 @@ combine_kernel(int nrec, int T2, const double *rec, double lam, int final_, doub
   __syncthreads();
   // 2. rescale factors exp(-(beta_r - beta)/lambda); Z, Z2
   double z = 0.0, z2 = 0.0;
-  for (int r = tid; r < nrec; r += kUpdThreads) {
+  for (int r = tid; r < nrec; r += kCombThreads) {
     const double *h = rec + (size_t)r * R;
     const double sc = (h[3] > 0.0) ? exp(-(h[0] - beta) / lam) : 0.0;
     s_scale[r] = sc;
@@ -162,7 +163,7 @@ combine_kernel(int nrec, int T2, const double *rec, double lam, int final_, doub
   }
   s_a[tid] = z; s_b[tid] = z2;
   __syncthreads();
-  for (int s = kUpdThreads / 2; s > 0; s >>= 1) {
+  for (int s = kCombThreads / 2; s > 0; s >>= 1) {
     if (tid < s) { s_a[tid] += s_a[tid + s]; s_b[tid] += s_b[tid + s]; }
     __syncthreads();
   }
@@ -177,17 +178,17 @@ combine_kernel(int nrec, int T2, const double *rec, double lam, int final_, doub
   //    summed in slice order (fixed order: deterministic).
   const int ns = max(1, min(kCombineSlices, min(kCombinePart / T2, nrec)));
   const int per = (nrec + ns - 1) / ns;
-  for (int it = tid; it < ns * T2; it += kUpdThreads) {
+  for (int it = tid; it < ns * T2; it += kCombThreads) {
     const int col = it % T2, sl = it / T2;
     const int r0 = sl * per, r1 = min(nrec, r0 + per);
     const double *src = rec + kRecHead + col;
     double a = 0.0;
-#pragma unroll 4
+#pragma unroll 16
     for (int r = r0; r < r1; ++r) a = fma(s_scale[r], src[(size_t)r * R], a);
     s_part[it] = a;
   }
   __syncthreads();
-  for (int col = tid; col < T2; col += kUpdThreads) {
+  for (int col = tid; col < T2; col += kCombThreads) {
     double a = 0.0;
     for (int sl = 0; sl < ns; ++sl) a += s_part[sl * T2 + col];
     if (!final_) {
@@ -204,7 +205,7 @@ combine_kernel(int nrec, int T2, const double *rec, double lam, int final_, doub
   }
   if (final_ && plan_out != nullptr) {
     __syncthreads();
-    for (int col = tid; col < T2; col += kUpdThreads) {
+    for (int col = tid; col < T2; col += kCombThreads) {
       const int src = (col + 2 < T2) ? col + 2 : col;   // drop first, repeat last
       plan_out[col] = (float)vplus[src];
     }
