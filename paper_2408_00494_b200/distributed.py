@@ -1,16 +1,18 @@
 """K-sharded BSS-MPPI across GPUs.
 
-Rollouts k are independent until the weighted update, so rank g of G owns a
+Rollouts k are independent until the weighted update, so rank r of N owns a
 contiguous k-range and computes, on its own GPU, the rollouts plus a partial
-record {beta_g = min finite cost, Z_g, Z2_g, n_g, argmin_g, N_g[T,2]} with
-weights relative to its own beta_g.  ONE collective per iteration -- an
-all-reduce(SUM) of a zero-initialised [G, 5 + 2T] FP64 buffer in which each
+record {beta_r = min finite cost, Z_r, Z2_r, n_r, argmin_r, N_r[T,2]} with
+weights relative to its own beta_r.  ONE collective per iteration -- an
+all-reduce(SUM) of a zero-initialised [N, 5 + 2T] FP64 buffer in which each
 rank fills only its slot (an all-gather in one all-reduce, 3.3 KB at T=50,
-G=8) -- then every rank combines the records in rank order on its device
-(rescaling by exp(-(beta_g - beta)/lambda)) and holds the identical v+.
+N=8) -- then every rank combines the records in rank order on its device
+(rescaling by exp(-(beta_r - beta)/lambda)) and holds the identical v+.
 
-Philox counters use the GLOBAL k, so every rollout is the same at any G and
-v+ differs from the single-GPU result only by FP64 summation order.
+Philox counters use the GLOBAL k, so every rollout draws the same noise at
+any N; v+ differs from the single-GPU result by FP64 summation order, and by
+FP32 summation order of the belief moments when a shard's lane-group width
+(chosen from its local rollout count) differs from the whole problem's.
 """
 
 from __future__ import annotations
