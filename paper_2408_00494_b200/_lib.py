@@ -26,6 +26,11 @@ class BssMppiError(RuntimeError):
         self.code = code
 
 
+class BssMppiUnsupported(BssMppiError, NotImplementedError):
+    """BSSMPPI_ERR_UNSUPPORTED: outside the device path (the reference's
+    NotImplementedError, INTEGRATION.md status table)."""
+
+
 class Problem(C.Structure):
     _fields_ = [
         ("kind", C.c_int32), ("samples", C.c_int32), ("horizon", C.c_int32),
@@ -116,7 +121,8 @@ def load():
 
 def check(code):
     if code != OK:
-        raise BssMppiError(code, load().bssmppi_last_error().decode())
+        cls = BssMppiUnsupported if code == ERR_UNSUPPORTED else BssMppiError
+        raise cls(code, load().bssmppi_last_error().decode())
     return code
 
 
