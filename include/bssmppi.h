@@ -27,6 +27,8 @@
  *   bssmppi_step_array        step_array (Euler)         dynamics.py:550-573
  *   bssmppi_enqueue_iteration device-resident control_step + warm start
  *                             (controllers.py:407-409, ControlPlan.shifted 154-156)
+ *   bssmppi_enqueue_step_device control_step on device buffers (torch tensors)
+ *                             controllers.py:374-410
  */
 #ifndef BSSMPPI_H
 #define BSSMPPI_H
@@ -165,6 +167,16 @@ int bssmppi_enqueue_partials(bssmppi_ctx *ctx, const uint32_t key_ctrl[2],
 int bssmppi_enqueue_combine(bssmppi_ctx *ctx, const double *partials_dev, int32_t nslots);
 /* Synchronise and read the last iteration's v+ (nullable) and diagnostics. */
 int bssmppi_download(bssmppi_ctx *ctx, double *vplus, bssmppi_diag *diag);
+
+/* One iteration on device buffers, for callers that keep the state on the
+ * GPU (e.g. torch CUDA tensors, with bssmppi_set_stream to torch's stream):
+ * state_dev = float x0[8] | cov0[16] (row-major 4x4) | plan[2T];
+ * out_dev   = double v+[2T] | head[5] {cost_min, Z, Z2, n_finite, argmin}.
+ * Asynchronous on the context stream: no host copies or synchronisation.
+ * n_finite == 0 in the head is the AllRolloutsInvalid case; state_dev is
+ * not modified (the caller does the warm-start shift). */
+int bssmppi_enqueue_step_device(bssmppi_ctx *ctx, const float *state_dev, const uint32_t key_ctrl[2],
+                                const uint32_t key_belief[2], double *out_dev);
 
 /* Rollout costs of a given sampled batch (rollout_bss / rollout_smppi /
  * rollout_mppi): u, eps (K*T*2, clamped / raw), nominal (T*2).

@@ -520,6 +520,32 @@ class Controller:
         dev = self._device_ctx()
         _lib.check(dev.lib.bssmppi_enqueue_iteration(dev.h, _lib.key_arr(key_ctrl), _lib.key_arr(key_belief)))
 
+    def step_device(self, state, out=None):
+        """One iteration on torch CUDA tensors, asynchronous on torch's current
+        stream (no host copies, no synchronisation) -- for callers that keep
+        the vehicle state on the GPU.  ``state``: float32 [8 + 16 + 2T]
+        (x0 | cov0 4x4 row-major | plan); returns float64 [2T + 5]
+        (v+ (T,2) flattened | cost_min, Z, Z2, n_finite, argmin).  Keys follow
+        ``self.iteration`` exactly as in ``control_step`` (which it then
+        advances); n_finite == 0 marks the AllRolloutsInvalid case, and the
+        warm-start shift of the plan is left to the caller."""
+        import torch
+        T = self.config.horizon
+        if self.noise_source != "philox":
+            raise ValueError("step_device uses the in-kernel Philox noise (noise_source='philox')")
+        if (not isinstance(state, torch.Tensor) or not state.is_cuda or state.dtype != torch.float32
+                or state.numel() != 24 + 2 * T or not state.is_contiguous()):
+            raise ValueError(f"state must be a contiguous float32 CUDA tensor of {24 + 2 * T} elements")
+        if out is None:
+            out = torch.empty(2 * T + 5, dtype=torch.float64, device=state.device)
+        dev = self._device_ctx()
+        _lib.check(dev.lib.bssmppi_set_stream(dev.h, _lib.C.c_void_p(torch.cuda.current_stream(state.device).cuda_stream)))
+        kc, kb = self._key(streams.DOMAIN_CONTROL), self._key(streams.DOMAIN_BELIEF)
+        _lib.check(dev.lib.bssmppi_enqueue_step_device(dev.h, _lib.C.c_void_p(state.data_ptr()), kc, kb,
+                                                       _lib.C.c_void_p(out.data_ptr())))
+        self.iteration += 1
+        return out
+
     def download(self):
         """Synchronise; (v+ (T,2), diagnostics dict) of the last iteration."""
         dev = self._device_ctx()

@@ -534,6 +534,24 @@ int bssmppi_download(bssmppi_ctx *c, double *vplus, bssmppi_diag *diag) {
   return finish(c, vplus, diag);
 }
 
+int bssmppi_enqueue_step_device(bssmppi_ctx *c, const float *state_dev, const uint32_t key_ctrl[2],
+                                const uint32_t key_belief[2], double *out_dev) {
+  if (!c) return fail(BSSMPPI_ERR_INVALID, "ctx is NULL");
+  if (!state_dev || !out_dev) return fail(BSSMPPI_ERR_INVALID, "state_dev and out_dev are required");
+  if (c->k_begin != 0 || c->k_count != c->K)
+    return fail(BSSMPPI_ERR_INVALID, "sharded context: use bssmppi_enqueue_partials + bssmppi_enqueue_combine");
+  DeviceGuard guard(c->device);
+  const int T2 = 2 * c->T;
+  CUDA_TRY(cudaMemcpyAsync(c->d_state, state_dev, (24 + T2) * sizeof(float), cudaMemcpyDeviceToDevice,
+                           c->stream));
+  RollParams rp = iteration_params(c, key_ctrl, key_belief);
+  int rc = run_iteration(c, rp, true, nullptr);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(out_dev, c->d_out, (T2 + kRecHead) * sizeof(double), cudaMemcpyDeviceToDevice,
+                           c->stream));
+  return BSSMPPI_OK;
+}
+
 int bssmppi_control_step(bssmppi_ctx *c, const double *x0, const double *cov0, const double *plan,
                          const uint32_t key_ctrl[2], const uint32_t key_belief[2], const double *eps,
                          const float *z, double *vplus, bssmppi_diag *diag) {

@@ -429,3 +429,29 @@ def test_update_golden_batch_shapes():
         v = mc.mppi_update(mc.RolloutBatch(controls, np.zeros_like(controls), costs), lam, mc.ControlBounds())
         np.testing.assert_allclose(v.controls, c_oracle.update(costs, controls, lam, [-0.35, -1], [0.35, 1]),
                                    atol=1e-12)
+
+
+def test_step_device_matches_control_step(oval, model):
+    """The device-buffer entry point (torch CUDA tensors in and out, no host
+    round trip) reproduces control_step bit for bit for the same seed,
+    run_path and iteration."""
+    import torch
+    cfg = mc.MppiConfig(kind="bss", samples=300, horizon=12, inner_samples=24,
+                        sigma_eps=np.diag([0.2 ** 2, 0.5 ** 2]))
+    noise = md.NoiseModel(np.diag([0.03 ** 2] * 3))
+    x0 = md.VehicleState.rolling(4.0, model, s=7.0).as_array()
+    host = mc.Controller(cfg, mc.CostSpec(), model, oval, noise=noise, seed=5, run_path=(5, 1))
+    dev = mc.Controller(cfg, mc.CostSpec(), model, oval, noise=noise, seed=5, run_path=(5, 1))
+    plan = np.zeros((cfg.horizon, 2))
+    for _ in range(3):
+        host.control_step(x0)
+        state = torch.tensor(np.concatenate([x0, np.zeros(16), plan.ravel()]), dtype=torch.float32, device="cuda")
+        out = dev.step_device(state)
+        torch.cuda.synchronize()
+        o = out.cpu().numpy()
+        np.testing.assert_array_equal(o[:2 * cfg.horizon].reshape(-1, 2), host.last_diagnostics["vplus"])
+        assert o[2 * cfg.horizon + 3] == host.last_diagnostics["n_finite"]
+        plan = np.concatenate([o[2:2 * cfg.horizon].reshape(-1, 2), o[2 * cfg.horizon - 2:2 * cfg.horizon][None]])
+    assert dev.iteration == host.iteration == 3
+    with pytest.raises(ValueError):
+        dev.step_device(torch.zeros(5, device="cuda"))
