@@ -87,6 +87,22 @@ CASES = [
     dict(name="c3_slice", track="spline0", K=32, M=256, T=50, dt=0.04, seed=0, run_path=[5, 0],
          warm=0, sigma_eps=ELLIPSE_SIGMA_EPS, noise=[0.05, 0.05, 0.05], x0="seeded",
          kind="bss", persist=False),
+    # rare branches of the step against the reference: the arc-length wrap
+    # (s just below L), the heading wrap (e_psi near pi, driving backwards
+    # along s so s also wraps below 0), the low-speed floor (vx < v_floor)
+    # and reverse driving (vx_eff < 0: the atan2 +-pi branch)
+    dict(name="s_wrap", track="oval", K=48, M=16, T=12, dt=0.05, seed=31, run_path=[6],
+         warm=1, sigma_eps=[[0.15 ** 2, 0], [0, 0.35 ** 2]], noise=[0.05, 0.05, 0.1],
+         x0=dict(vx=5.0, s_frac=0.995, e_y=0.2), kind="bss", persist=False),
+    dict(name="heading_wrap", track="oval", K=48, M=16, T=12, dt=0.05, seed=32, run_path=[6],
+         warm=0, sigma_eps=[[0.15 ** 2, 0], [0, 0.35 ** 2]], noise=[0.05, 0.05, 0.1],
+         x0=dict(vx=2.0, s_frac=0.002, e_psi=3.05, e_y=-0.3), kind="bss", persist=False),
+    dict(name="low_speed", track="ellipse", K=48, M=16, T=12, dt=0.05, seed=33, run_path=[6],
+         warm=1, sigma_eps=[[0.15 ** 2, 0], [0, 0.35 ** 2]], noise=[0.02, 0.02, 0.05],
+         x0=dict(vx=0.15, s=10.0), kind="bss", persist=False),
+    dict(name="reverse", track="ellipse", K=48, M=16, T=10, dt=0.05, seed=34, run_path=[6],
+         warm=0, sigma_eps=[[0.15 ** 2, 0], [0, 0.35 ** 2]], noise=[0.02, 0.02, 0.05],
+         x0=dict(vx=-2.0, s=20.0, e_y=0.2), plan=[0.05, -0.5], kind="bss", persist=False),
     # deterministic kinds through the same kernel
     dict(name="smppi", track="oval", K=48, M=1, T=10, dt=0.05, seed=11, run_path=[],
          warm=2, sigma_eps=[[0.15 ** 2, 0], [0, 0.35 ** 2]], noise=[0.0, 0.0, 0.0],
@@ -125,6 +141,8 @@ def build(case, mods):
     else:
         kw = dict(case["x0"])
         vx = kw.pop("vx")
+        if "s_frac" in kw:
+            kw["s"] = kw.pop("s_frac") * track.length
         x0 = mods.VehicleState.rolling(vx, model, **kw).as_array()
     cov0 = np.asarray(case.get("cov0", np.zeros((4, 4))), dtype=float)
     cfg = mods.MppiConfig(kind=case["kind"], samples=case["K"], horizon=case["T"],
