@@ -103,6 +103,15 @@ CASES = [
     dict(name="reverse", track="ellipse", K=48, M=16, T=10, dt=0.05, seed=34, run_path=[6],
          warm=0, sigma_eps=[[0.15 ** 2, 0], [0, 0.35 ** 2]], noise=[0.02, 0.02, 0.05],
          x0=dict(vx=-2.0, s=20.0, e_y=0.2), plan=[0.05, -0.5], kind="bss", persist=False),
+    # every cost term away from its default: all eight tracking weights,
+    # goal speed, lane-exit penalty, terminal scale, CBF rate / penalty and
+    # back-off (controllers.py:108-138, constraints.py:22-33)
+    dict(name="custom_cost", track="ellipse", K=64, M=24, T=15, dt=0.05, seed=35, run_path=[7],
+         warm=1, sigma_eps=[[0.2 ** 2, 0], [0, 0.5 ** 2]], noise=[0.03, 0.03, 0.06],
+         x0=dict(vx=4.5, s=12.0, e_y=0.9, e_psi=0.05), kind="bss", persist=False,
+         cost=dict(q_diag=[3.0, 0.5, 0.1, 1e-4, 2e-4, 1.5, 0.8, 0.01], v_goal=4.0,
+                   obstacle_penalty=500.0, terminal_scale=3.0,
+                   safety=dict(cbf_rate=0.2, penalty=700.0), backoff=2.5)),
     # deterministic kinds through the same kernel
     dict(name="smppi", track="oval", K=48, M=1, T=10, dt=0.05, seed=11, run_path=[],
          warm=2, sigma_eps=[[0.15 ** 2, 0], [0, 0.35 ** 2]], noise=[0.0, 0.0, 0.0],
@@ -150,7 +159,12 @@ def build(case, mods):
                           sigma_eps=np.asarray(case["sigma_eps"], dtype=float),
                           inner_samples=max(case["M"], 2),
                           persist_particles=case["persist"])
-    cost = mods.CostSpec()
+    cost_kw = dict(case.get("cost", {}))
+    if "safety" in cost_kw:
+        cost_kw["safety"] = mods.SafetyParams(**cost_kw["safety"])
+    if "q_diag" in cost_kw:
+        cost_kw["q_diag"] = np.asarray(cost_kw["q_diag"], dtype=float)
+    cost = mods.CostSpec(**cost_kw)
     plan = None
     if "plan" in case:
         plan = np.tile(np.asarray(case["plan"], dtype=float), (case["T"], 1))

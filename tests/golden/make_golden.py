@@ -34,10 +34,12 @@ from belief_mppi.streams import substream  # noqa: E402
 from cases import CASES, CLOSED_LOOP, UPDATE_BATCHES, build, build_closed_loop, update_batch  # noqa: E402
 from belief_mppi import sim as rsim  # noqa: E402
 
+from belief_mppi.constraints import SafetyParams as RefSafetyParams  # noqa: E402
+
 REF = types.SimpleNamespace(
     VehicleParams=rd.VehicleParams, VehicleState=rd.VehicleState, NoiseModel=rd.NoiseModel,
     CostSpec=rc.CostSpec, MppiConfig=rc.MppiConfig, make_test_track=rd.make_test_track,
-    with_timestep=rd.with_timestep)
+    with_timestep=rd.with_timestep, SafetyParams=RefSafetyParams)
 
 
 def noise_checksums(case, it):

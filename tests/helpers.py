@@ -14,10 +14,12 @@ from paper_2408_00494_b200 import dynamics as md
 
 GOLDEN = Path(__file__).resolve().parent / "golden"
 
+from paper_2408_00494_b200.constraints import SafetyParams  # noqa: E402
+
 MINE = types.SimpleNamespace(
     VehicleParams=md.VehicleParams, VehicleState=md.VehicleState, NoiseModel=md.NoiseModel,
     CostSpec=mc.CostSpec, MppiConfig=mc.MppiConfig, make_test_track=md.make_test_track,
-    with_timestep=md.with_timestep)
+    with_timestep=md.with_timestep, SafetyParams=SafetyParams)
 
 
 def load_golden(name):
