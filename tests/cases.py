@@ -112,6 +112,21 @@ CASES = [
          cost=dict(q_diag=[3.0, 0.5, 0.1, 1e-4, 2e-4, 1.5, 0.8, 0.01], v_goal=4.0,
                    obstacle_penalty=500.0, terminal_scale=3.0,
                    safety=dict(cbf_rate=0.2, penalty=700.0), backoff=2.5)),
+    # every vehicle parameter away from its default (the 23-value physics
+    # vector: mass, inertia, geometry, wheels, all eight magic-formula B/C,
+    # the four peaks, drive gain, rolling resistance, low-speed floor)
+    dict(name="custom_vehicle", track="oval", K=64, M=24, T=15, dt=0.04, seed=36, run_path=[7],
+         warm=1, sigma_eps=[[0.2 ** 2, 0], [0, 0.5 ** 2]], noise=[0.03, 0.03, 0.06],
+         x0=dict(vx=3.5, s=8.0, e_y=-0.4), kind="bss", persist=False,
+         vehicle=dict(mass=18.0, inertia_z=0.9, lf=0.22, lr=0.28, wheel_radius=0.11, wheel_inertia=0.3,
+                      b_lat_front=5.0, c_lat_front=1.4, b_lat_rear=3.5, c_lat_rear=1.2,
+                      b_long_front=2.5, c_long_front=1.6, b_long_rear=1.8, c_long_rear=1.5,
+                      peak_fx_front=90.0, peak_fy_front=100.0, peak_fx_rear=110.0, peak_fy_rear=95.0,
+                      drive_gain=10.0, roll_resist=0.02, v_floor=0.4)),
+    # an open track: the arc length clamps at L instead of wrapping
+    dict(name="open_track", track="open60", K=48, M=16, T=15, dt=0.05, seed=37, run_path=[7],
+         warm=1, sigma_eps=[[0.15 ** 2, 0], [0, 0.35 ** 2]], noise=[0.03, 0.03, 0.06],
+         x0=dict(vx=5.0, s=57.0, e_y=0.2), kind="bss", persist=False),
     # deterministic kinds through the same kernel
     dict(name="smppi", track="oval", K=48, M=1, T=10, dt=0.05, seed=11, run_path=[],
          warm=2, sigma_eps=[[0.15 ** 2, 0], [0, 0.35 ** 2]], noise=[0.0, 0.0, 0.0],
@@ -135,8 +150,14 @@ def build(case, mods):
     make_test_track, with_timestep)."""
     from paper_2408_00494_b200.tracks import named_track
 
-    track = named_track(case["track"], build=mods.make_test_track)
-    model = mods.with_timestep(mods.VehicleParams(), case["dt"], "euler")
+    if case["track"] == "open60":
+        # an open (non-closing) track: s is clamped to [0, L] instead of wrapped
+        s_pts = np.linspace(0.0, 60.0, 121)
+        track = mods.Track(s=s_pts, kappa=0.03 * np.sin(s_pts / 9.0), half_width=2.0, closed=False,
+                           length=60.0)
+    else:
+        track = named_track(case["track"], build=mods.make_test_track)
+    model = mods.with_timestep(mods.VehicleParams(**case.get("vehicle", {})), case["dt"], "euler")
     stds, s0 = _seeded_scalars(case["seed"], track.length)
     nz = case["noise"]
     if nz == "seeded":

@@ -39,7 +39,7 @@ from belief_mppi.constraints import SafetyParams as RefSafetyParams  # noqa: E40
 REF = types.SimpleNamespace(
     VehicleParams=rd.VehicleParams, VehicleState=rd.VehicleState, NoiseModel=rd.NoiseModel,
     CostSpec=rc.CostSpec, MppiConfig=rc.MppiConfig, make_test_track=rd.make_test_track,
-    with_timestep=rd.with_timestep, SafetyParams=RefSafetyParams)
+    with_timestep=rd.with_timestep, SafetyParams=RefSafetyParams, Track=rd.Track)
 
 
 def noise_checksums(case, it):
