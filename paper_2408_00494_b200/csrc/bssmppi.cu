@@ -196,6 +196,7 @@ int build_track(bssmppi_ctx *c, const bssmppi_problem *p) {
   tr.node = c->d_node;
   tr.cell = c->d_cell;
   tr.L = Lf;
+  tr.L2 = 2.f * Lf;
   tr.inv_h = (float)(1.0 / h);
   tr.half_width = (float)p->half_width;
   tr.ncell = ncell;
@@ -217,6 +218,9 @@ void fill_params(bssmppi_ctx *c, const bssmppi_problem *p) {
   V.spin_scale = (float)(q[4] / 0.1); V.dt = (float)p->dt;
   V.lf_nlr = make_float2(V.lf, -V.lr);
   V.By_s = make_float2(V.Byf, -V.Byr);
+  V.nBy = make_float2(-V.Byf, -V.Byr);
+  V.dt_lf_iz = (float)(p->dt * q[2] / q[1]);
+  V.ndt_lr_iz = (float)(-p->dt * q[3] / q[1]);
   V.Cy = make_float2(V.Cyf, V.Cyr);
   V.Dy = make_float2(V.Dyf, V.Dyr);
   V.Bx = make_float2(V.Bxf, V.Bxr);

@@ -73,6 +73,29 @@ __device__ __forceinline__ float2 atan_x2(float2 x) {
   return make_float2(copysignf(tx > 1.f ? q.x : p.x, x.x), copysignf(ty > 1.f ? q.y : p.y, x.y));
 }
 
+// atan2(Y, X) of two arguments given x = Y / X (via the caller's shared
+// reciprocal of X) and rev = (1, 0) for X > 0, (-1, pi) for X < 0:
+// sign(Y) (rev.y + rev.x atan|x|) -- the left-half-plane shift folded into
+// one FFMA2 (bit-identical to atan(x) + copysign(pi, Y) there, and to
+// atan(x) itself for X > 0).
+__device__ __forceinline__ float2 atan2_x2(float2 x, float2 Y, float2 rev) {
+  const float tx = fabsf(x.x), ty = fabsf(x.y);
+  const float2 a = make_float2(fminf(tx, rcp_approx(tx)), fminf(ty, rcp_approx(ty)));
+  const float2 s = __fmul2_rn(a, a);
+  float2 p = __ffma2_rn(s, bc2(-4.822528455e-03f), bc2(2.473404258e-02f));
+  p = __ffma2_rn(p, s, bc2(-6.020310149e-02f));
+  p = __ffma2_rn(p, s, bc2(9.968471527e-02f));
+  p = __ffma2_rn(p, s, bc2(-1.404132694e-01f));
+  p = __ffma2_rn(p, s, bc2(1.997421384e-01f));
+  p = __ffma2_rn(p, s, bc2(-3.333239257e-01f));
+  p = __fmul2_rn(p, s);
+  p = __ffma2_rn(a, p, a);
+  const float2 q = __fadd2_rn(bc2(1.57079637f), make_float2(-p.x, -p.y));
+  const float2 base = make_float2(tx > 1.f ? q.x : p.x, ty > 1.f ? q.y : p.y);
+  const float2 mag = __ffma2_rn(bc2(rev.x), base, bc2(rev.y));
+  return make_float2(copysignf(mag.x, Y.x), copysignf(mag.y, Y.y));
+}
+
 // sin and cos of one argument in one packed Horner chain: lane x runs the
 // sine polynomial (padded with a leading 0, so it is evaluated exactly as
 // the scalar Horner), lane y the cosine; coefficients as in sincos_pi.
@@ -97,9 +120,12 @@ __device__ __forceinline__ float2 sin_pi_x2(float2 x) {
   return __fmul2_rn(p, x);
 }
 
-// returns (sin x, cos x), any x (reduced to [-pi, pi] as in sincos_pi)
+// returns (sin x, cos x), any x: reduced to [-pi, pi] as in sincos_pi, but
+// unconditionally -- for |x| <= pi, n = 0 and x passes through unchanged --
+// so the particle step carries neither a compare nor predicated reduction
+// instructions (A/B: 4 straight-line instructions beat the guarded form)
 __device__ __forceinline__ float2 sincos_pi_x2(float x) {
-  if (fabsf(x) > 3.14159265f) {
+  {
     const float n = rintf(x * 0.159154943f);
     x = fmaf(-n, 6.28318548e+00f, x);
     x = fmaf(n, 1.74845553e-07f, x);

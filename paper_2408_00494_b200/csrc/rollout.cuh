@@ -103,7 +103,7 @@ __device__ __forceinline__ float shield_penalty(float hc, float hp, const RollPa
 // inside = some d_i < r_i (collision indicator of the stage cost).
 __device__ __forceinline__ float obstacle_terms(const RollParams &P, float s, float ey, float sigy,
                                                 bool &inside) {
-  const float sw = P.tr.closed ? floor_mod(s, P.tr.L) : fminf(fmaxf(s, 0.f), P.tr.L);
+  const float sw = track_s(s, P.tr);
   const float fi = sw * P.cl_inv_ds;
   const int j = min(max((int)fi, 0), P.cl_n - 2);
   const float f = fi - (float)j;
@@ -282,7 +282,10 @@ __device__ __forceinline__ void group_allreduce18(float a[18], int li, float *sl
 }
 
 constexpr int kSlotFloats = 20;   // 18 sums, 16-byte aligned slot
-constexpr int kBlockThreads = 128;
+#ifndef BSS_BLOCK_THREADS
+#define BSS_BLOCK_THREADS 128
+#endif
+constexpr int kBlockThreads = BSS_BLOCK_THREADS;
 // Register budget: 4 resident 128-thread blocks per SM (<= 128 registers,
 // 16 warps/SM).  With the software-pipelined noise (particle_pass) the extra
 // registers buy more than occupancy: 5 / 6 / 7 blocks per SM (96 / 80 / 72
@@ -329,14 +332,20 @@ __device__ __forceinline__ float control_prologue(const RollParams &P, int k, in
   return cc;
 }
 
+// Process-noise kinds of the particle loop (template parameter NK): diagonal
+// Gaussian factor (3 multiplies, the hot case), a general 3x3 factor or none
+// (the reference skips the add, dynamics.py:571; a runtime test), config-4
+// Laplace + slip.
+enum NoiseKind { NK_GAUSS_DIAG = 0, NK_LAPLACE = 1, NK_GAUSS_GENERAL = 2 };
+
 // The 7 noise values of particle-step (t, k, m): [0:4] the re-projection
 // normals on the tracked subset, [4:7] the process noise -- standard
 // normals scaled by F after the step (the column layout of the reference's
 // z_all block, controllers.py:285-287, belief.py:328-333) or, for the
 // config-4 extension, the Laplace + slip increments themselves.  ZARR reads
 // the reference's normals (guarded to zeros for m >= M).  NK, the noise
-// kind (0 Gaussian, 1 Laplace + slip), is a template parameter so that the
-// pipelined loop body of particle_pass is one scheduling region.
+// kind (NoiseKind), is a template parameter so that the pipelined loop body
+// of particle_pass is one branch-free scheduling region.
 template <bool ZARR, int NK>
 __device__ __forceinline__ void particle_noise(const RollParams &P, int t, int k, int kg, int m, float n[7]) {
   if (ZARR) {
@@ -352,7 +361,7 @@ __device__ __forceinline__ void particle_noise(const RollParams &P, int t, int k
   } else {
     Philox4 a, b;
     belief_bits(P.kb, (uint32_t)t, (uint32_t)kg, (uint32_t)m, a, b);
-    if (NK == 1) laplace_from_bits(a, b, P.lap_b, P.slip_a, n, n + 4);
+    if (NK == NK_LAPLACE) laplace_from_bits(a, b, P.lap_b, P.slip_a, n, n + 4);
     else normals_from_bits(a, b, n);
   }
 }
@@ -380,15 +389,15 @@ __device__ __forceinline__ void particle_step(const RollParams &P, int t, int m,
   // shares (vx, omega_f, omega_r, s) with the mean, hence the shared terms
   if (PERSIST && t > 0) vehicle_step(x, ctl, P.V, P.tr);
   else step_particle(x, sh, ctl, P.V, P.tr);
-  if (NK == 1) {                         // config-4 extension, after integration too
+  if (NK == NK_LAPLACE) {                // config-4 extension, after integration too
     x[0] += z[4];
     x[1] += z[5];
     x[2] += z[6];
-  } else if (P.noise_diag) {             // added after integration (dynamics.py:571-572)
+  } else if (NK == NK_GAUSS_DIAG) {      // added after integration (dynamics.py:571-572)
     x[0] = fmaf(P.F[0], z[4], x[0]);
     x[1] = fmaf(P.F[4], z[5], x[1]);
     x[2] = fmaf(P.F[8], z[6], x[2]);
-  } else if (P.noise_on) {
+  } else if (P.noise_on) {               // NK_GAUSS_GENERAL: 3x3 factor or none
     x[0] += P.F[0] * z[4] + P.F[1] * z[5] + P.F[2] * z[6];
     x[1] += P.F[3] * z[4] + P.F[4] * z[5] + P.F[5] * z[6];
     x[2] += P.F[6] * z[4] + P.F[7] * z[5] + P.F[8] * z[6];
@@ -458,9 +467,11 @@ __device__ __forceinline__ void particle_pass(const RollParams &P, int t, int k,
 
 // BSS rollouts.  G: lanes per rollout; PERSIST: keep the particle cloud in
 // shared memory instead of re-projecting (controllers.py:288-305);
-// ZARR: read the reference's normals instead of Philox.
-template <int G, bool PERSIST, bool ZARR>
-__global__ void __launch_bounds__(kBlockThreads, BSS_MIN_BLOCKS) bss_rollout_kernel(const RollParams P) {
+// ZARR: read the reference's normals instead of Philox; NK: the process
+// noise kind (NoiseKind), resolved once at kernel entry so every variant's
+// T loop holds exactly one particle loop (register allocation per variant).
+template <int G, bool PERSIST, bool ZARR, int NK>
+__device__ __forceinline__ void bss_rollout(const RollParams &P) {
   extern __shared__ float4 smem4[];
   float *smem = reinterpret_cast<float *>(smem4);
   constexpr int GPW = 32 / G;
@@ -511,10 +522,7 @@ __global__ void __launch_bounds__(kBlockThreads, BSS_MIN_BLOCKS) bss_rollout_ker
 #pragma unroll
     for (int i = 0; i < 18; ++i) acc[i] = 0.f;
     float c[8];
-    if (!ZARR && P.noise_kind == 1)
-      particle_pass<G, PERSIST, ZARR, 1>(P, t, k, kg, li, mean, L, ctl, sh, cloud, acc, c);
-    else
-      particle_pass<G, PERSIST, ZARR, 0>(P, t, k, kg, li, mean, L, ctl, sh, cloud, acc, c);
+    particle_pass<G, PERSIST, ZARR, NK>(P, t, k, kg, li, mean, L, ctl, sh, cloud, acc, c);
     group_allreduce18<G>(acc, li, slots + (t & 1) * kSlotFloats);
 
     // moments (belief.py:275-308 semantics)
@@ -565,6 +573,18 @@ __global__ void __launch_bounds__(kBlockThreads, BSS_MIN_BLOCKS) bss_rollout_ker
   total += P.term * stage_cost(mean, P) + shield_penalty(h_cur, h_prev, P);
   if (P.n_obs) total += P.term * (inside ? P.c_obs : 0.f) + shield_penalty(ho_cur, ho_prev, P);
   if (active && li == 0) P.cost_out[k] = dead ? __int_as_float(0x7f800000) : total;
+}
+
+#ifdef BSS_MAXNREG
+#define BSS_ROLLOUT_BOUNDS __maxnreg__(BSS_MAXNREG)
+#else
+#define BSS_ROLLOUT_BOUNDS __launch_bounds__(kBlockThreads, BSS_MIN_BLOCKS)
+#endif
+template <int G, bool PERSIST, bool ZARR>
+__global__ void BSS_ROLLOUT_BOUNDS bss_rollout_kernel(const RollParams P) {
+  if (!ZARR && P.noise_kind == 1) bss_rollout<G, PERSIST, ZARR, NK_LAPLACE>(P);
+  else if (P.noise_diag) bss_rollout<G, PERSIST, ZARR, NK_GAUSS_DIAG>(P);
+  else bss_rollout<G, PERSIST, ZARR, NK_GAUSS_GENERAL>(P);
 }
 
 // Deterministic rollouts for kind "mppi" / "smppi" (controllers.py:320-338):

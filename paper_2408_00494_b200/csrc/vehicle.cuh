@@ -40,6 +40,8 @@ struct VehDev {
   float2 By_s;     // (Byf, -Byr): B alpha with alpha_r = -atan2(.) folded in
   float2 Cy, Dy;   // (Cyf, Cyr), (Dyf, Dyr)
   float2 Bx, Cx;   // (Bxf, Bxr), (Cxf, Cxr): longitudinal pair of step_shared
+  float2 nBy;      // (-Byf, -Byr): the lateral-slip pair as one FFMA2 on (atan2 f, atan2 r)
+  float dt_lf_iz, ndt_lr_iz;   // dt lf / Iz, -dt lr / Iz: the yaw-rate Euler update
 };
 
 // node[j] = {s_j, kappa_j, slope_j, s_{j+1}} plus a sentinel node[n].
@@ -48,6 +50,7 @@ struct TrackDev {
   const int *cell;
   float L, inv_h, half_width;
   int ncell, n, closed;
+  float L2;   // 2 L: upper end of the exact floor-mod fast path
 };
 
 struct CtlDev {
@@ -83,8 +86,25 @@ __device__ __forceinline__ float wrap_pi(float a) {
   return wrap_pi_slow(a);
 }
 
+// Arc length after a step: the Python floor-mod on a closed track
+// (dynamics.py:486-489), a clamp to [0, L] on an open one.  Both are the
+// identity on [0, L) -- every particle-step except a lap crossing -- which is
+// tested first; the closed-track fast path (exact on [-L, 2L)) and the
+// out-of-line fmodf / clamp follow only when that test fails.
+__device__ __noinline__ float track_s_slow(float x, float L, int closed) {
+  return closed ? floor_mod(x, L) : fminf(fmaxf(x, 0.f), L);
+}
+
+__device__ __forceinline__ float track_s(float x, const TrackDev &tr) {
+  const float L = tr.L;
+  const float r = (x >= L) ? x - L : ((x < 0.f) ? x + L : x);
+  if (__builtin_expect(x >= 0.f && x < L, 1)) return x;
+  if (__builtin_expect(tr.closed && x >= -L && x < tr.L2, 1)) return r;
+  return track_s_slow(x, L, tr.closed);
+}
+
 __device__ __forceinline__ float curvature(const TrackDev &tr, float s) {
-  const float sw = tr.closed ? floor_mod(s, tr.L) : fminf(fmaxf(s, 0.f), tr.L);
+  const float sw = track_s(s, tr);
   int ci = __float2int_rz(sw * tr.inv_h);
   ci = min(max(ci, 0), tr.ncell - 1);
   int lo = __ldg(tr.cell + ci);
@@ -159,6 +179,8 @@ struct StepShared {
   float2 fb0;                 // (fxf cd + fxr, fxf sd): the particle-independent
                               //   parts of the body-frame force sums
   float2 nsd_cd;              // (-sin delta, cos delta)
+  float2 rev;                 // atan2 quadrant fold: (1, 0) for vx_eff > 0, (-1, pi) below
+  float2 byd;                 // (Byf delta, 0): front slip-angle offset of the lateral pair
 };
 
 __device__ __forceinline__ StepShared step_shared(const float x[8], const CtlDev &c, const VehDev &V,
@@ -203,6 +225,8 @@ __device__ __forceinline__ StepShared step_shared(const float x[8], const CtlDev
   h.dvx_lon = h.fxr;
   h.fb0 = make_float2(fmaf(h.fxf, c.cd, h.fxr), h.fxf * c.sd);
   h.nsd_cd = make_float2(-c.sd, c.cd);
+  h.rev = (h.vxe >= 0.f) ? make_float2(1.f, 0.f) : make_float2(-1.f, 3.14159265358979f);
+  h.byd = make_float2(V.Byf * c.delta, 0.f);
   // _derivs_row wheel torque balance; rolling resistance opposes the spin
 #ifdef BSS_EXACT_MATH
   const float spf = tanhf(wf * V.spin_scale), spr = tanhf(wr * V.spin_scale);
@@ -253,7 +277,7 @@ __device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, c
   x[5] = wrap_pi(ep + V.dt * dep);
   x[6] = ey + V.dt * dey;
   const float s1 = s + V.dt * ds;
-  x[7] = tr.closed ? floor_mod(s1, tr.L) : fminf(fmaxf(s1, 0.f), tr.L);
+  x[7] = track_s(s1, tr);
   if (__builtin_expect(!all_finite8(x), 0)) ok = scrub_nonfinite(x) && ok;
   return ok;
 }
@@ -270,20 +294,16 @@ __device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, c
   // slip-angle numerators (vy + lf r, vy - lr r); atan2(., vxe) = atan(. / vxe)
   // for vxe > 0, +-pi shifted for vxe < 0 (vxe is shared by the rollout)
   const float2 Y = __ffma2_rn(bc2(r), V.lf_nlr, bc2(vy));
-  float2 A = atan_x2(__fmul2_rn(Y, bc2(h.rx)));
-  if (h.vxe < 0.f) {
-    A.x += copysignf(3.14159265358979f, Y.x);
-    A.y += copysignf(3.14159265358979f, Y.y);
-  }
-  // (B_f alpha_f, B_r alpha_r), alpha_f = delta - A.x, alpha_r = -A.y
-  const float2 ty = __fmul2_rn(V.Cy, atan_x2(__fmul2_rn(V.By_s, make_float2(c.delta - A.x, A.y))));
+  const float2 A = atan2_x2(__fmul2_rn(Y, bc2(h.rx)), Y, h.rev);
+  // (B_f alpha_f, B_r alpha_r) = (Byf delta - Byf A.x, -Byr A.y): alpha_f =
+  // delta - A.x, alpha_r = -A.y
+  const float2 ty = __fmul2_rn(V.Cy, atan_x2(__ffma2_rn(V.nBy, A, h.byd)));
   // |ty| < C pi / 2 <= pi (lateral C <= 2, checked at context creation)
   const float2 fy = __fmul2_rn(__fmul2_rn(V.Dy, sin_pi_x2(ty)), h.cx);
   // body-frame front force + rear longitudinal: (fxf cd - fyf sd + fxr, fxf sd + fyf cd)
   const float2 fb = __ffma2_rn(bc2(fy.x), h.nsd_cd, h.fb0);
   // (dvx, dvy) = (fb.x, fb.y + fyr) / m + (vy r, -vx r)
   const float2 dv = __ffma2_rn(make_float2(fb.x, fb.y + fy.y), bc2(V.inv_m), make_float2(vy * r, -(vx * r)));
-  const float dr = (V.lf * fb.y - V.lr * fy.y) * V.inv_iz;
   float frame = 1.f - h.kap * ey;
   bool ok = frame > 0.f;
   if (frame < 1e-3f) frame = 1e-3f;
@@ -303,13 +323,13 @@ __device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, c
   const float2 v56 = __ffma2_rn(bc2(V.dt), make_float2(dep, dey), make_float2(ep, ey));
   x[0] = v01.x;
   x[1] = v01.y;
-  x[2] = fmaf(V.dt, dr, r);
+  x[2] = fmaf(V.dt_lf_iz, fb.y, fmaf(V.ndt_lr_iz, fy.y, r));   // r + dt (lf fyb - lr fyr) / Iz
   x[3] = h.wf1;
   x[4] = h.wr1;
   x[5] = wrap_pi(v56.x);
   x[6] = v56.y;
   const float s1 = fmaf(V.dt, ds, s);
-  x[7] = tr.closed ? floor_mod(s1, tr.L) : fminf(fmaxf(s1, 0.f), tr.L);
+  x[7] = track_s(s1, tr);
   if (__builtin_expect(!all_finite8(x), 0)) ok = scrub_nonfinite(x) && ok;
   return ok;
 }

@@ -41,3 +41,4 @@ run("C2", 4096, 128, 40, 0.05, "ellipse")
 run("C3", 16384, 256, 50, 0.04, "spline0")
 run("C5a", 4096, 512, 60, 0.04, "spline0")
 run("C5b", 32768, 64, 60, 0.04, "spline0")
+run("S8", 2048, 256, 50, 0.04, "spline0")
