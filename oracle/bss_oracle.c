@@ -195,6 +195,13 @@ static void control_normals(uint32_t k0, uint32_t k1, uint32_t t, uint32_t kg, d
   bm(a[0], a[1], z0, z1);
 }
 
+/* The 7 belief normals of (t, kg, m) for m < m_count (row-major [m][7]): the
+ * checker for bssmppi_belief_normals. */
+int orc_belief_normals(const uint32_t key[2], uint32_t t, uint32_t kg, int m_count, double *out) {
+  for (int m = 0; m < m_count; ++m) belief_normals(key[0], key[1], t, kg, (uint32_t)m, out + (size_t)m * 7);
+  return 0;
+}
+
 /* Per-iteration key (same definition as bssmppi_iteration_key). */
 int orc_iteration_key(const uint32_t base[2], uint32_t domain, uint64_t iteration, uint32_t out[2]) {
   uint32_t c[4] = {(uint32_t)iteration, (uint32_t)(iteration >> 32), domain, 0x6b657973u};

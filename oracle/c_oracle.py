@@ -33,6 +33,7 @@ def load():
         lib.orc_control_step.argtypes = [C.POINTER(Problem), _dp, _dp, _dp, _u32p, _u32p, _dp, _dp,
                                          _dp, C.c_int]
         lib.orc_philox4x32.argtypes = [_u32p, _u32p, C.c_int, _u32p]
+        lib.orc_belief_normals.argtypes = [_u32p, C.c_uint32, C.c_uint32, C.c_int, _dp]
         lib.orc_max_threads.restype = C.c_int
         lib.orc_iteration_key.argtypes = [_u32p, C.c_uint32, C.c_uint64, _u32p]
         _lib = lib
@@ -96,6 +97,13 @@ def philox(ctr, key, rounds=10):
     out = (C.c_uint32 * 4)()
     load().orc_philox4x32((C.c_uint32 * 4)(*ctr), (C.c_uint32 * 2)(*key), int(rounds), out)
     return list(out)
+
+
+def belief_normals(key, t, kg, m_count):
+    """(m_count, 7) FP64 belief normals of particle-steps (t, kg, m < m_count)."""
+    out = np.empty((m_count, 7))
+    load().orc_belief_normals((C.c_uint32 * 2)(*key), int(t), int(kg), int(m_count), _p(out))
+    return out
 
 
 def iteration_key(base, domain, iteration):

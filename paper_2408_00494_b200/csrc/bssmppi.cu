@@ -236,7 +236,11 @@ void fill_params(bssmppi_ctx *c, const bssmppi_problem *p) {
   for (int i = 0; i < 4; ++i) { r.prec[i] = (float)p->precision[i]; r.sfac[i] = (float)p->sigma_factor[i]; }
   for (int i = 0; i < 2; ++i) { r.lo[i] = (float)p->bounds_lo[i]; r.hi[i] = (float)p->bounds_hi[i]; }
   bool any = false;
-  for (int i = 0; i < 9; ++i) { r.F[i] = (float)p->noise_factor[i]; any |= p->noise_factor[i] != 0.0; }
+  for (int i = 0; i < 9; ++i) {
+    r.F[i] = (float)p->noise_factor[i];
+    r.Fk[i] = (float)((double)kBmNeg * p->noise_factor[i]);
+    any |= p->noise_factor[i] != 0.0;
+  }
   r.noise_on = any ? 1 : 0;
   const double *F = p->noise_factor;
   r.noise_diag = (any && F[1] == 0.0 && F[2] == 0.0 && F[3] == 0.0 && F[5] == 0.0 && F[6] == 0.0 &&

@@ -80,25 +80,41 @@ __device__ __forceinline__ float lg2_approx(float x) {
   return y;
 }
 
-// Box-Muller pair from two 32-bit words.  Uniforms are built by bit
-// insertion (no I2F on the XU pipe): u1 in (0, 1], angle in [-pi, pi).
-__device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float &z0, float &z1) {
+// Box-Muller in the units the MUFU pipe works in.  The reference-side form
+// (oracle/bss_oracle.c bm) is r (cos, sin)(2 pi (m_b - 1.5)) with
+// r = sqrt(-2 ln u1), u1 = 2 - m_a and m_a, m_b in [1, 2) the mantissa values
+// of the two words' top 23 bits (uniforms by bit insertion, no I2F).  Since
+// sqrt(-2 ln u) = sqrt(2 ln 2) sqrt(-log2 u) and (cos, sin)(2 pi (m - 1.5)) =
+// -(cos, sin)(2 pi m), the pair is kBmNeg * raw with
+//   raw = sqrt(-log2 u1) (cos, sin)(2 pi m_b),
+// which costs no multiply for the ln 2 factor (the negation is a MUFU
+// operand modifier) and one FMUL by an immediate for the angle.  The rollout
+// folds kBmNeg into its Cholesky and process-noise factors; everything else
+// (statistics kernel, control samples) scales back with box_muller().
+constexpr float kBmNeg = -1.17741002251547469f;   // -sqrt(2 ln 2)
+
+__device__ __forceinline__ void box_muller_raw(uint32_t a, uint32_t b, float &z0, float &z1) {
   const float u1 = 2.0f - __uint_as_float(0x3f800000u | (a >> 9));
-  // angle 2 pi (m - 1.5) for the mantissa value m in [1, 2): one FFMA
-  const float ang = fmaf(__uint_as_float(0x3f800000u | (b >> 9)), 6.28318530718f, -9.42477796077f);
-  const float r = sqrt_approx(-1.38629436112f * lg2_approx(u1));  // sqrt(-2 ln u1)
+  const float ang = __uint_as_float(0x3f800000u | (b >> 9)) * 6.28318530718f;
+  const float r = sqrt_approx(-lg2_approx(u1));
   float s, c;
   __sincosf(ang, &s, &c);
   z0 = r * c;
   z1 = r * s;
 }
 
-// Single normal (cosine branch) of a Box-Muller pair.
-__device__ __forceinline__ void box_muller1(uint32_t a, uint32_t b, float &z0) {
+// Single raw normal (cosine branch) of a pair.
+__device__ __forceinline__ void box_muller_raw1(uint32_t a, uint32_t b, float &z0) {
   const float u1 = 2.0f - __uint_as_float(0x3f800000u | (a >> 9));
-  const float ang = fmaf(__uint_as_float(0x3f800000u | (b >> 9)), 6.28318530718f, -9.42477796077f);
-  const float r = sqrt_approx(-1.38629436112f * lg2_approx(u1));
-  z0 = r * __cosf(ang);
+  const float ang = __uint_as_float(0x3f800000u | (b >> 9)) * 6.28318530718f;
+  z0 = sqrt_approx(-lg2_approx(u1)) * __cosf(ang);
+}
+
+// Standard normal pair (the oracle's bm()).
+__device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float &z0, float &z1) {
+  box_muller_raw(a, b, z0, z1);
+  z0 *= kBmNeg;
+  z1 *= kBmNeg;
 }
 
 // The 7 standard normals of particle-step (t, k, m) (Philox4x32-7 counters): [0:4] re-projection
@@ -112,18 +128,22 @@ __device__ __forceinline__ void belief_bits(const PhiloxKeys &rk, uint32_t t, ui
   b = philox4x32<kBeliefRounds>(Philox4{t, m, kg, 1u}, rk);
 }
 
-__device__ __forceinline__ void normals_from_bits(const Philox4 &a, const Philox4 &b, float z[7]) {
-  box_muller(a.x, a.y, z[0], z[1]);
-  box_muller(a.z, a.w, z[2], z[3]);
-  box_muller(b.x, b.y, z[4], z[5]);
-  box_muller1(b.z, b.w, z[6]);
+// The 7 raw normals (standard normals / kBmNeg) of a particle-step.
+__device__ __forceinline__ void raw_normals_from_bits(const Philox4 &a, const Philox4 &b, float z[7]) {
+  box_muller_raw(a.x, a.y, z[0], z[1]);
+  box_muller_raw(a.z, a.w, z[2], z[3]);
+  box_muller_raw(b.x, b.y, z[4], z[5]);
+  box_muller_raw1(b.z, b.w, z[6]);
 }
 
+// The 7 standard normals of particle-step (t, k, m) (statistics / parity kernel).
 __device__ __forceinline__ void belief_normals(const PhiloxKeys &rk, uint32_t t, uint32_t kg,
                                                uint32_t m, float z[7]) {
   Philox4 a, b;
   belief_bits(rk, t, kg, m, a, b);
-  normals_from_bits(a, b, z);
+  raw_normals_from_bits(a, b, z);
+#pragma unroll
+  for (int j = 0; j < 7; ++j) z[j] *= kBmNeg;
 }
 
 // Config-4 extension: 4 re-projection normals + Laplace(0, b) on (vx, vy, r)
@@ -136,10 +156,11 @@ __device__ __forceinline__ float centred_uniform2(uint32_t w) {
   return fmaf(__uint_as_float(0x3f800000u | (w >> 9)), 2.0f, -3.0f) + 1.1920928955078125e-07f;
 }
 
+// z[0:4] are RAW normals (x kBmNeg = standard), w the noise increments.
 __device__ __forceinline__ void laplace_from_bits(const Philox4 &p, const Philox4 &q, float b, float a,
                                                   float z[4], float w[3]) {
-  box_muller(p.x, p.y, z[0], z[1]);
-  box_muller(p.z, p.w, z[2], z[3]);
+  box_muller_raw(p.x, p.y, z[0], z[1]);
+  box_muller_raw(p.z, p.w, z[2], z[3]);
   const uint32_t words[3] = {q.x, q.y, q.z};
 #pragma unroll
   for (int i = 0; i < 3; ++i) {

@@ -49,6 +49,7 @@ struct RollParams {
   float v_goal, c_obs, term, beta1 /* 1 - beta */, c_pen, nu;
   float gamma, prec[4], sfac[4], lo[2], hi[2];
   float F[9];          // process-noise factor
+  float Fk[9];         // kBmNeg * F: the factor applied to Philox raw normals (philox.cuh)
   int chol_rank;       // max Cholesky rank: min(4, M - 1) (cov0: 4)
   PhiloxKeys kc;       // control-noise key schedule
   PhiloxKeys kb;       // belief-noise key schedule
@@ -223,6 +224,13 @@ __device__ __forceinline__ void chol4(const float C[10], float L[10], int max_ra
   L[5] = l22; L[6] = l30; L[7] = l31; L[8] = l32; L[9] = l33;
 }
 
+// The re-projection factor for Philox raw normals: L kBmNeg (philox.cuh),
+// once per (k, t) instead of one multiply per normal.
+__device__ __forceinline__ void scale_raw(float L[10]) {
+#pragma unroll
+  for (int i = 0; i < 10; ++i) L[i] *= kBmNeg;
+}
+
 // Reduce-scatter butterfly of 18 partial sums over a G-lane group, then an
 // all-gather through shared memory; every lane returns the 18 group sums.
 template <int G>
@@ -362,17 +370,18 @@ __device__ __forceinline__ void particle_noise(const RollParams &P, int t, int k
     Philox4 a, b;
     belief_bits(P.kb, (uint32_t)t, (uint32_t)kg, (uint32_t)m, a, b);
     if (NK == NK_LAPLACE) laplace_from_bits(a, b, P.lap_b, P.slip_a, n, n + 4);
-    else normals_from_bits(a, b, n);
+    else raw_normals_from_bits(a, b, n);
   }
 }
 
 // One particle-step given its noise: re-project (or load the persistent
 // particle), Euler step, process noise.  Returns the post-step state in x.
-template <bool PERSIST, int NK>
+template <bool PERSIST, bool ZARR, int NK>
 __device__ __forceinline__ void particle_step(const RollParams &P, int t, int m, const float mean[8],
                                               const float L[10], const CtlDev &ctl, const StepShared &sh,
                                               float *cloud, const float z[7], float x[8]) {
   const int M = P.M;
+  const float *F = ZARR ? P.F : P.Fk;   // Philox normals arrive raw (x kBmNeg folded in)
   if (PERSIST && t > 0) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) x[i] = cloud[i * M + m];
@@ -394,13 +403,13 @@ __device__ __forceinline__ void particle_step(const RollParams &P, int t, int m,
     x[1] += z[5];
     x[2] += z[6];
   } else if (NK == NK_GAUSS_DIAG) {      // added after integration (dynamics.py:571-572)
-    x[0] = fmaf(P.F[0], z[4], x[0]);
-    x[1] = fmaf(P.F[4], z[5], x[1]);
-    x[2] = fmaf(P.F[8], z[6], x[2]);
+    x[0] = fmaf(F[0], z[4], x[0]);
+    x[1] = fmaf(F[4], z[5], x[1]);
+    x[2] = fmaf(F[8], z[6], x[2]);
   } else if (P.noise_on) {               // NK_GAUSS_GENERAL: 3x3 factor or none
-    x[0] += P.F[0] * z[4] + P.F[1] * z[5] + P.F[2] * z[6];
-    x[1] += P.F[3] * z[4] + P.F[4] * z[5] + P.F[5] * z[6];
-    x[2] += P.F[6] * z[4] + P.F[7] * z[5] + P.F[8] * z[6];
+    x[0] += F[0] * z[4] + F[1] * z[5] + F[2] * z[6];
+    x[1] += F[3] * z[4] + F[4] * z[5] + F[5] * z[6];
+    x[2] += F[6] * z[4] + F[7] * z[5] + F[8] * z[6];
   }
   if (PERSIST) {
 #pragma unroll
@@ -447,7 +456,7 @@ __device__ __forceinline__ void particle_pass(const RollParams &P, int t, int k,
   float x[8], zc[7], zn[7];
   particle_noise<ZARR, NK>(P, t, k, kg, li, zc);
   if (li + G < M) particle_noise<ZARR, NK>(P, t, k, kg, li + G, zn);
-  if (has0) particle_step<PERSIST, NK>(P, t, li, mean, L, ctl, sh, cloud, zc, x);
+  if (has0) particle_step<PERSIST, ZARR, NK>(P, t, li, mean, L, ctl, sh, cloud, zc, x);
 #pragma unroll
   for (int i = 0; i < 8; ++i) c[i] = __shfl_sync(0xffffffffu, x[i], 0, G);
   if (has0) accumulate<!PERSIST>(acc, x, c);
@@ -456,11 +465,11 @@ __device__ __forceinline__ void particle_pass(const RollParams &P, int t, int k,
 #pragma unroll
     for (int j = 0; j < 7; ++j) zc[j] = zn[j];
     particle_noise<ZARR, NK>(P, t, k, kg, m + G, zn);
-    particle_step<PERSIST, NK>(P, t, m, mean, L, ctl, sh, cloud, zc, x);
+    particle_step<PERSIST, ZARR, NK>(P, t, m, mean, L, ctl, sh, cloud, zc, x);
     accumulate<!PERSIST>(acc, x, c);
   }
   if (m < M) {                            // last particle: no look-ahead draw
-    particle_step<PERSIST, NK>(P, t, m, mean, L, ctl, sh, cloud, zn, x);
+    particle_step<PERSIST, ZARR, NK>(P, t, m, mean, L, ctl, sh, cloud, zn, x);
     accumulate<!PERSIST>(acc, x, c);
   }
 }
@@ -498,6 +507,7 @@ __device__ __forceinline__ void bss_rollout(const RollParams &P) {
     for (int i = 0; i < 10; ++i) C[i] = P.cov0[ui[i]];
   }
   chol4(C, L, 4);   // the initial belief covariance is not a sample estimate
+  if (!ZARR) scale_raw(L);
   float h_cur = dcbf(mean[6], sigma_of(C[9]), P);
   float h_prev = h_cur;
   bool inside = false;
@@ -568,7 +578,10 @@ __device__ __forceinline__ void bss_rollout(const RollParams &P) {
       ho_prev = ho_cur;
       ho_cur = obstacle_terms(P, mean[7], mean[6], sigma_of(C[9]), inside);
     }
-    if (!PERSIST) chol4(C, L, P.chol_rank);
+    if (!PERSIST) {
+      chol4(C, L, P.chol_rank);
+      if (!ZARR) scale_raw(L);
+    }
   }
   total += P.term * stage_cost(mean, P) + shield_penalty(h_cur, h_prev, P);
   if (P.n_obs) total += P.term * (inside ? P.c_obs : 0.f) + shield_penalty(ho_cur, ho_prev, P);

@@ -85,6 +85,19 @@ def test_belief_normals_statistics():
     assert np.array_equal(z, z2)
 
 
+def test_belief_normals_match_oracle():
+    """Device Box-Muller (MUFU lg2/sqrt/sin/cos on the raw form, kBmNeg
+    scale) equals the FP64 oracle's bm() on the same Philox words."""
+    lib = _lib.load()
+    n = 1 << 14
+    z = np.empty((n, 7), dtype=np.float32)
+    _lib.check(lib.bssmppi_belief_normals(_lib.key_arr((12345, 678)), 3, 77, n, _lib.fptr(z)))
+    ref = c_oracle.belief_normals((12345, 678), 3, 77, n)
+    err = np.abs(z - ref)
+    assert err.max() < 3e-5, err.max()
+    assert np.median(err) < 1e-6, np.median(err)
+
+
 # ------------------------------------------------------------ dynamics
 
 def test_step_array_matches_oracle(oval, model):
