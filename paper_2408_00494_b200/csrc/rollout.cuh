@@ -461,6 +461,9 @@ __device__ __forceinline__ void particle_pass(const RollParams &P, int t, int k,
   for (int i = 0; i < 8; ++i) c[i] = __shfl_sync(0xffffffffu, x[i], 0, G);
   if (has0) accumulate<!PERSIST>(acc, x, c);
   int m = li + G;
+  // unrolled twice: the look-ahead noise alternates between two register
+  // sets instead of being copied (7 moves) at every particle
+#pragma unroll 2
   for (; m + G < M; m += G) {             // steady state: look one particle ahead
 #pragma unroll
     for (int j = 0; j < 7; ++j) zc[j] = zn[j];

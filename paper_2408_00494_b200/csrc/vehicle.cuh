@@ -123,11 +123,14 @@ __device__ __forceinline__ float curvature(const TrackDev &tr, float s) {
 
 // Non-finite components -> 0 (dynamics.py:493-496); returns "all finite".
 // Inlined into the cold branch: an out-of-line call taking x by address
-// would pin the particle state in local memory for the whole loop.
-__device__ __forceinline__ bool scrub_nonfinite(float *x) {
+// would pin the particle state in local memory for the whole loop.  The
+// wheel speeds x[3], x[4] are shared by a rollout's particles and scrubbed
+// once per (k, t) in step_shared, so only the other six are visited here.
+__device__ __forceinline__ bool scrub_nonfinite6(float *x) {
   bool fin = true;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
+    if (i == 3 || i == 4) continue;
     fin &= isfinite(x[i]);
     x[i] = isfinite(x[i]) ? x[i] : 0.f;
   }
@@ -161,6 +164,14 @@ __device__ __forceinline__ bool all_finite2(float a, float b) {
   return max2_nan(fabsf(a), fabsf(b)) < __int_as_float(0x7f800000);
 }
 
+// x[0..2], x[5..7] (the particle-dependent components after a step)
+__device__ __forceinline__ bool finite6(const float x[8]) {
+  float m = max3_nan(fabsf(x[0]), fabsf(x[1]), fabsf(x[2]));
+  m = max3_nan(m, fabsf(x[5]), fabsf(x[6]));
+  m = max2_nan(m, fabsf(x[7]));
+  return m < __int_as_float(0x7f800000);
+}
+
 // The step split in two: everything that depends only on (vx, omega_f,
 // omega_r, s) and the control -- the longitudinal slips and tire forces,
 // the wheel accelerations and kappa(s) -- is `step_shared`; the rest, which
@@ -174,7 +185,8 @@ struct StepShared {
   float fxf, fxr;             // longitudinal forces
   float2 cx;                  // (front, rear) |cos| friction-ellipse factors
   float dvx_lon;              // (fxr) / m: rear longitudinal force term of dvx
-  float wf1, wr1;             // next-step wheel speeds (omega + dt * d omega)
+  float wf1, wr1;             // next-step wheel speeds (omega + dt * d omega), non-finite -> 0
+  bool wfin;                  // both wheel speeds were finite (part of the step's ok)
   float kap;                  // kappa(s)
   float2 fb0;                 // (fxf cd + fxr, fxf sd): the particle-independent
                               //   parts of the body-frame force sums
@@ -237,6 +249,11 @@ __device__ __forceinline__ StepShared step_shared(const float x[8], const CtlDev
   const float dwr = (c.drive_u1 - V.R * h.fxr - V.rrr * spr) * V.inv_jw;
   h.wf1 = wf + V.dt * dwf;
   h.wr1 = wr + V.dt * dwr;
+  h.wfin = all_finite2(h.wf1, h.wr1);
+  if (__builtin_expect(!h.wfin, 0)) {   // _step_kernel scrub of the shared components
+    h.wf1 = isfinite(h.wf1) ? h.wf1 : 0.f;
+    h.wr1 = isfinite(h.wr1) ? h.wr1 : 0.f;
+  }
   h.kap = curvature(tr, s);
   return h;
 }
@@ -278,8 +295,8 @@ __device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, c
   x[6] = ey + V.dt * dey;
   const float s1 = s + V.dt * ds;
   x[7] = track_s(s1, tr);
-  if (__builtin_expect(!all_finite8(x), 0)) ok = scrub_nonfinite(x) && ok;
-  return ok;
+  if (__builtin_expect(!finite6(x), 0)) ok = scrub_nonfinite6(x) && ok;
+  return ok && h.wfin;
 }
 
 #else
@@ -297,7 +314,7 @@ __device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, c
   const float2 A = atan2_x2(__fmul2_rn(Y, bc2(h.rx)), Y, h.rev);
   // (B_f alpha_f, B_r alpha_r) = (Byf delta - Byf A.x, -Byr A.y): alpha_f =
   // delta - A.x, alpha_r = -A.y
-  const float2 ty = __fmul2_rn(V.Cy, atan_x2(__ffma2_rn(V.nBy, A, h.byd)));
+  const float2 ty = __fmul2_rn(V.Cy, atan_x2(make_float2(fmaf(V.nBy.x, A.x, h.byd.x), V.nBy.y * A.y)));
   // |ty| < C pi / 2 <= pi (lateral C <= 2, checked at context creation)
   const float2 fy = __fmul2_rn(__fmul2_rn(V.Dy, sin_pi_x2(ty)), h.cx);
   // body-frame front force + rear longitudinal: (fxf cd - fyf sd + fxr, fxf sd + fyf cd)
@@ -330,8 +347,8 @@ __device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, c
   x[6] = v56.y;
   const float s1 = fmaf(V.dt, ds, s);
   x[7] = track_s(s1, tr);
-  if (__builtin_expect(!all_finite8(x), 0)) ok = scrub_nonfinite(x) && ok;
-  return ok;
+  if (__builtin_expect(!finite6(x), 0)) ok = scrub_nonfinite6(x) && ok;
+  return ok && h.wfin;
 }
 #endif
 
