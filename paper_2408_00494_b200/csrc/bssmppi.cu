@@ -197,6 +197,9 @@ int build_track(bssmppi_ctx *c, const bssmppi_problem *p) {
   tr.cell = c->d_cell;
   tr.L = Lf;
   tr.L2 = 2.f * Lf;
+  // smallest float with Lf * s_scale >= 2 exactly (products of floats are exact in double)
+  tr.s_scale = (float)(2.0 / (double)Lf);
+  while ((double)Lf * (double)tr.s_scale < 2.0) tr.s_scale = std::nextafter(tr.s_scale, INFINITY);
   tr.inv_h = (float)(1.0 / h);
   tr.half_width = (float)p->half_width;
   tr.ncell = ncell;

@@ -51,6 +51,7 @@ struct TrackDev {
   float L, inv_h, half_width;
   int ncell, n, closed;
   float L2;   // 2 L: upper end of the exact floor-mod fast path
+  float s_scale;   // 2 / L rounded up (common_case: |s s_scale - 1| < 1 implies 0 < s < L)
 };
 
 struct CtlDev {
@@ -92,7 +93,8 @@ __device__ __forceinline__ float wrap_pi(float a) {
 // tested first; the closed-track fast path (exact on [-L, 2L)) and the
 // out-of-line fmodf / clamp follow only when that test fails.
 __device__ __noinline__ float track_s_slow(float x, float L, int closed) {
-  return closed ? floor_mod(x, L) : fminf(fmaxf(x, 0.f), L);
+  if (closed) return floor_mod(x, L);
+  return x < 0.f ? 0.f : (x > L ? L : x);   // NaN stays NaN (then scrubbed, ok = false)
 }
 
 __device__ __forceinline__ float track_s(float x, const TrackDev &tr) {
@@ -170,6 +172,27 @@ __device__ __forceinline__ bool finite6(const float x[8]) {
   m = max3_nan(m, fabsf(x[5]), fabsf(x[6]));
   m = max2_nan(m, fabsf(x[7]));
   return m < __int_as_float(0x7f800000);
+}
+
+// One screen for the rare events at the end of a step (dynamics.py:479-496):
+// an arc-length wrap (closed track) or clamp (open track) and a non-finite
+// component.  True only if neither can occur: 0 < s < L (tr.s_scale = 2/L
+// rounded up, so s >= L always fails) and the other components finite (their
+// max, scaled by 2^-126, stays below 1; NaN and inf fail, as do magnitudes
+// >= 2^126, which then take the exact path).  One max.NaN chain and one
+// branch instead of two guarded branches.  The heading wrap keeps its own
+// early test (wrap_pi): folding it in as well measured slower (profiles/).
+__device__ __forceinline__ bool common_case(const float x[8], const TrackDev &tr) {
+  const float m = max3_nan(max3_nan(fabsf(x[0]), fabsf(x[1]), fabsf(x[2])), fabsf(x[6]), fabsf(x[5])) * 0x1p-126f;
+  const float sv = fmaf(x[7], tr.s_scale, -1.f);
+  return max2_nan(m, fabsf(sv)) < 1.f;
+}
+
+// The exact per-component treatment when common_case fails: arc-length
+// wrap / clamp, then non-finite -> 0; returns "all finite".
+__device__ __forceinline__ bool rare_fixup(float x[8], const TrackDev &tr) {
+  x[7] = track_s(x[7], tr);
+  return finite6(x) || scrub_nonfinite6(x);
 }
 
 // The step split in two: everything that depends only on (vx, omega_f,
@@ -345,9 +368,8 @@ __device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, c
   x[4] = h.wr1;
   x[5] = wrap_pi(v56.x);
   x[6] = v56.y;
-  const float s1 = fmaf(V.dt, ds, s);
-  x[7] = track_s(s1, tr);
-  if (__builtin_expect(!finite6(x), 0)) ok = scrub_nonfinite6(x) && ok;
+  x[7] = fmaf(V.dt, ds, s);
+  if (__builtin_expect(!common_case(x, tr), 0)) ok = rare_fixup(x, tr) && ok;
   return ok && h.wfin;
 }
 #endif

@@ -129,6 +129,74 @@ def test_step_array_matches_oracle(oval, model):
     dc.close()
 
 
+def _f32_track_s(s, L, closed):
+    """float32 emulation of the device arc-length wrap (vehicle.cuh track_s:
+    Python floor-mod on a closed track, exact on [-L, 2L) and fmodf beyond;
+    clamp on an open one)."""
+    f = np.float32
+    s, L = f(s), f(L)
+    if not closed:   # reference: s < 0 -> 0, s > L -> L, NaN passes (dynamics.py:488-491)
+        return s if np.isnan(s) else f(min(max(s, f(0)), L))
+    if not np.isfinite(s):
+        return f(np.nan)
+    if f(0) <= s < L:
+        return s
+    if L <= s < f(2) * L:
+        return f(s - L)
+    if -L <= s < f(0):
+        return f(s + L)
+    r = f(np.fmod(s, L))
+    return f(r + L) if r < 0 else r
+
+
+@pytest.mark.parametrize("closed", [True, False])
+def test_step_array_rare_events(model, closed):
+    """The step's rare-event screen (vehicle.cuh common_case + rare_fixup,
+    wrap_pi) at its exact boundaries: with vx = vy = r = 0 the arc length and
+    heading pass through the Euler update unchanged, so the device output is
+    the wrap of the float32 input (dynamics.py:479-496 semantics)."""
+    segs = named_track("oval")
+    if closed:
+        track = segs
+    else:
+        track = md.Track(segs.s, segs.kappa, segs.half_width, closed=False, length=segs.s[-1] + 1.0)
+    f = np.float32
+    L = f(track.length)
+    ulp = np.spacing(L)
+    s_in = [0.0, 1e-30, L / 2, L - ulp, L, L + ulp, f(1.5) * L, -ulp, f(-1.0), f(-0.5) * L,
+            f(2.5) * L, f(-3.25) * L, np.inf, np.nan]
+    pi = f(np.pi)
+    e_in = [0.0, np.nextafter(pi, f(0)), pi, np.nextafter(pi, f(4)), -pi, np.nextafter(-pi, f(0)),
+            f(4.0), f(-4.0), f(1e3)]
+    rows = [(sv, 0.0) for sv in s_in] + [(10.0, ev) for ev in e_in]
+    n = len(rows)
+    x = np.zeros((n, 8))
+    x[:, 7] = [r[0] for r in rows]
+    x[:, 5] = [r[1] for r in rows]
+    x[:, 6] = 0.1
+    u = np.zeros((n, 2))
+    ctx = mc.RolloutContext(model, track, mc.CostSpec())
+    prob, keep = mc.build_problem("mppi", 1, 1, 1, 1.0, 0.0, np.eye(2), None, mc.ControlBounds(),
+                                  False, ctx)
+    dc = mc.DeviceContext(prob)
+    out = np.empty_like(x)
+    ok = np.empty(n, dtype=np.uint8)
+    _lib.check(dc.lib.bssmppi_step_array(dc.h, n, _lib.dptr(x), _lib.dptr(u), None, _lib.dptr(out),
+                                         ok.ctypes.data_as(_lib.C.POINTER(_lib.C.c_uint8))))
+    dc.close()
+    for i, (sv, ev) in enumerate(rows):
+        exp_s = _f32_track_s(sv, L, closed)
+        if np.isnan(exp_s):        # non-finite -> 0 and the step is not ok
+            assert out[i, 7] == 0.0 and not ok[i], (sv, out[i])
+            continue
+        assert f(out[i, 7]) == exp_s, (sv, out[i, 7], exp_s)
+        e = f(ev)
+        exp_e = e if -pi < e <= pi else f(pi - _f32_track_s(f(pi - e), f(2 * np.pi), True))
+        assert f(out[i, 5]) == exp_e, (ev, out[i, 5], exp_e)
+        assert -pi <= out[i, 5] <= pi
+        assert ok[i]
+
+
 # ------------------------------------------------------------ update law
 # (reference test_controllers.py:86-147)
 
