@@ -228,7 +228,7 @@ __device__ __forceinline__ StepShared step_shared(const float x[8], const CtlDev
   h.rx = 1.0f / h.vxe;
   h.inv_den = 1.0f / fabsf(h.vxe);
 #else
-  h.rx = __frcp_rn(h.vxe);           // |vxe| >= v_floor > 0
+  h.rx = rcp_approx(h.vxe);          // |vxe| >= v_floor > 0: MUFU.RCP, 1 ulp
   h.inv_den = fabsf(h.rx);
 #endif
   const float sgf = (wf * V.R - vx) * h.inv_den;
