@@ -74,6 +74,49 @@ def atan32(coef, x):
     return np.copysign(p, x)
 
 
+def fit_atan_rat(n_p=3, n_q=2, iters=80):
+    """atan(a) = a P(s) / Q(s), s = a^2, a in [0, 1], Q monic of degree n_q:
+    Loeb's linearisation (P - g Q_low = g s^n_q, re-weighted by 1 / Q) with
+    Lawson weights, minimax in the relative error.  Coefficients lowest first."""
+    a = np.cos(np.linspace(np.pi / 2, 0, 40001)) ** 0.5
+    a = a[a > 1e-5]
+    s = a * a
+    g = np.arctan(a) / a
+    q_val = np.ones_like(s)
+    ww = np.ones_like(s)
+    for _ in range(iters):
+        basis = np.concatenate([np.stack([s ** k for k in range(n_p + 1)], 1),
+                                -g[:, None] * np.stack([s ** k for k in range(n_q)], 1)], 1)
+        sw = np.sqrt(ww) / (np.abs(q_val) * g)
+        c, *_ = np.linalg.lstsq(basis * sw[:, None], g * s ** n_q * sw, rcond=None)
+        p, q = c[:n_p + 1], np.append(c[n_p + 1:], 1.0)
+        q_val = sum(q[k] * s ** k for k in range(n_q + 1))
+        err = np.abs(sum(p[k] * s ** k for k in range(n_p + 1)) / q_val - g) / g
+        ww = ww * err
+        ww /= ww.sum()
+    return f32(p), f32(q)
+
+
+def atan_rat32(p, q, x):
+    """Device algorithm of fastmath.cuh atan_mag_x2 + sign: a = min(|x|, 1/|x|),
+    P, Q Horner (Q's monic top step an add), R = 1/Q (MUFU.RCP modelled as
+    correctly rounded), r = fma(+-a, P R, 0 or pi/2), sign of x."""
+    t = np.abs(x)
+    with np.errstate(divide="ignore"):
+        a = np.minimum(t, f32(1.0 / t))
+    s = f32(a * a)
+    P = np.full_like(s, p[-1])
+    for ck in p[-2::-1]:
+        P = fma32(P, s, ck)
+    Q = f32(s + q[-2])
+    for ck in q[-3::-1]:
+        Q = fma32(Q, s, ck)
+    PR = f32(P * f32(1.0 / Q))
+    big = t > 1.0
+    r = fma32(np.where(big, -a, a), PR, np.where(big, np.float32(1.57079637), 0.0))
+    return np.copysign(r, x)
+
+
 def check_atan(coef):
     x = f32(np.concatenate([np.linspace(-40, 40, 2000001), np.geomspace(1e-6, 1e6, 400001)]))
     y = atan32(coef, x)
@@ -85,6 +128,16 @@ def check_atan(coef):
 
 def main():
     what = sys.argv[1] if len(sys.argv) > 1 else "atan"
+    if what == "atan_rat":
+        p, q = fit_atan_rat()
+        x = f32(np.concatenate([np.linspace(-40, 40, 2000001), np.geomspace(1e-6, 1e6, 400001)]))
+        ex = np.arctan(x)
+        e = np.abs(atan_rat32(p, q, x) - ex)
+        ulp = np.spacing(np.abs(ex).astype(np.float32)).astype(np.float64)
+        print(f"(3,2) rational: max abs err {e.max():.3e}, {(e / ulp).max():.2f} ulp")
+        print("  P (lowest first):", ", ".join(f"{v:.9e}f" for v in p))
+        print("  Q (lowest first):", ", ".join(f"{v:.9e}f" for v in q))
+        return
     if what == "atan":
         for deg in (6, 7):
             c = fit_atan(deg)
