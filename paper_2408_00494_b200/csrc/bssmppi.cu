@@ -197,9 +197,6 @@ int build_track(bssmppi_ctx *c, const bssmppi_problem *p) {
   tr.cell = c->d_cell;
   tr.L = Lf;
   tr.L2 = 2.f * Lf;
-  // smallest float with Lf * s_scale >= 2 exactly (products of floats are exact in double)
-  tr.s_scale = (float)(2.0 / (double)Lf);
-  while ((double)Lf * (double)tr.s_scale < 2.0) tr.s_scale = std::nextafter(tr.s_scale, INFINITY);
   tr.inv_h = (float)(1.0 / h);
   tr.half_width = (float)p->half_width;
   tr.ncell = ncell;
@@ -224,6 +221,7 @@ void fill_params(bssmppi_ctx *c, const bssmppi_problem *p) {
   V.nBy = make_float2(-V.Byf, -V.Byr);
   V.dt_lf_iz = (float)(p->dt * q[2] / q[1]);
   V.ndt_lr_iz = (float)(-p->dt * q[3] / q[1]);
+  V.dt_m = (float)(p->dt / q[0]);
   V.Cy = make_float2(V.Cyf, V.Cyr);
   V.Dy = make_float2(V.Dyf, V.Dyr);
   V.Bx = make_float2(V.Bxf, V.Bxr);

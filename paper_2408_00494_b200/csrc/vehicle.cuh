@@ -42,6 +42,7 @@ struct VehDev {
   float2 Bx, Cx;   // (Bxf, Bxr), (Cxf, Cxr): longitudinal pair of step_shared
   float2 nBy;      // (-Byf, -Byr): the lateral-slip pair as one FFMA2 on (atan2 f, atan2 r)
   float dt_lf_iz, ndt_lr_iz;   // dt lf / Iz, -dt lr / Iz: the yaw-rate Euler update
+  float dt_m;                  // dt / m: the (vx, vy) Euler update
 };
 
 // node[j] = {s_j, kappa_j, slope_j, s_{j+1}} plus a sentinel node[n].
@@ -51,7 +52,6 @@ struct TrackDev {
   float L, inv_h, half_width;
   int ncell, n, closed;
   float L2;   // 2 L: upper end of the exact floor-mod fast path
-  float s_scale;   // 2 / L rounded up (common_case: |s s_scale - 1| < 1 implies 0 < s < L)
 };
 
 struct CtlDev {
@@ -176,16 +176,14 @@ __device__ __forceinline__ bool finite6(const float x[8]) {
 
 // One screen for the rare events at the end of a step (dynamics.py:479-496):
 // an arc-length wrap (closed track) or clamp (open track) and a non-finite
-// component.  True only if neither can occur: 0 < s < L (tr.s_scale = 2/L
-// rounded up, so s >= L always fails) and the other components finite (their
-// max, scaled by 2^-126, stays below 1; NaN and inf fail, as do magnitudes
-// >= 2^126, which then take the exact path).  One max.NaN chain and one
-// branch instead of two guarded branches.  The heading wrap keeps its own
+// component.  True only if neither can occur: 0 <= s < L (both the floor-mod
+// and the clamp are the identity there) and the other components finite
+// (their max.NaN is below inf).  Compares and max chains only -- ALU work,
+// no FMA-pipe cycle -- feeding one branch.  The heading wrap keeps its own
 // early test (wrap_pi): folding it in as well measured slower (profiles/).
 __device__ __forceinline__ bool common_case(const float x[8], const TrackDev &tr) {
-  const float m = max3_nan(max3_nan(fabsf(x[0]), fabsf(x[1]), fabsf(x[2])), fabsf(x[6]), fabsf(x[5])) * 0x1p-126f;
-  const float sv = fmaf(x[7], tr.s_scale, -1.f);
-  return max2_nan(m, fabsf(sv)) < 1.f;
+  const float m = max3_nan(max3_nan(fabsf(x[0]), fabsf(x[1]), fabsf(x[2])), fabsf(x[6]), fabsf(x[5]));
+  return (m < __int_as_float(0x7f800000)) & (x[7] >= 0.f) & (x[7] < tr.L);
 }
 
 // The exact per-component treatment when common_case fails: arc-length
@@ -342,8 +340,6 @@ __device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, c
   const float2 fy = __fmul2_rn(__fmul2_rn(V.Dy, sin_pi_x2(ty)), h.cx);
   // body-frame front force + rear longitudinal: (fxf cd - fyf sd + fxr, fxf sd + fyf cd)
   const float2 fb = __ffma2_rn(bc2(fy.x), h.nsd_cd, h.fb0);
-  // (dvx, dvy) = (fb.x, fb.y + fyr) / m + (vy r, -vx r)
-  const float2 dv = __ffma2_rn(make_float2(fb.x, fb.y + fy.y), bc2(V.inv_m), make_float2(vy * r, -(vx * r)));
   float frame = 1.f - h.kap * ey;
   bool ok = frame > 0.f;
   if (frame < 1e-3f) frame = 1e-3f;
@@ -359,10 +355,12 @@ __device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, c
   const float dey = fmaf(vx, sc.x, vsc.y);
   const float dep = fmaf(-h.kap, ds, r);
   // _step_kernel Euler branch + wraps
-  const float2 v01 = __ffma2_rn(bc2(V.dt), dv, make_float2(vx, vy));
+  // (vx, vy) + dt ((fb.x, fb.y + fyr) / m + (vy r, -vx r)) with dt / m and
+  // dt r folded into the FMAs: 6 FMA-pipe cycles instead of 7
+  const float dtr = V.dt * r;
   const float2 v56 = __ffma2_rn(bc2(V.dt), make_float2(dep, dey), make_float2(ep, ey));
-  x[0] = v01.x;
-  x[1] = v01.y;
+  x[0] = fmaf(V.dt_m, fb.x, fmaf(dtr, vy, vx));
+  x[1] = fmaf(V.dt_m, fb.y, fmaf(V.dt_m, fy.y, fmaf(-dtr, vx, vy)));
   x[2] = fmaf(V.dt_lf_iz, fb.y, fmaf(V.ndt_lr_iz, fy.y, r));   // r + dt (lf fyb - lr fyr) / Iz
   x[3] = h.wf1;
   x[4] = h.wr1;
