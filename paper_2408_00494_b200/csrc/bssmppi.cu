@@ -222,6 +222,7 @@ void fill_params(bssmppi_ctx *c, const bssmppi_problem *p) {
   V.dt_lf_iz = (float)(p->dt * q[2] / q[1]);
   V.ndt_lr_iz = (float)(-p->dt * q[3] / q[1]);
   V.dt_m = (float)(p->dt / q[0]);
+  V.tire_short = std::max(q[7], q[9]) * (M_PI / 2.0) <= 2.2 ? 1 : 0;
   V.Cy = make_float2(V.Cyf, V.Cyr);
   V.Dy = make_float2(V.Dyf, V.Dyr);
   V.Bx = make_float2(V.Bxf, V.Bxr);

@@ -120,6 +120,24 @@ __device__ __forceinline__ float2 sin_pi_x2(float2 x) {
   return __fmul2_rn(p, x);
 }
 
+// sin of two magic-formula arguments, |x| <= 2.2 (lateral shape factors
+// C <= 1.40, incl. the reference default 1.3): sin x = x (1 + t Q(t)),
+// t = x^2, Q of degree 4 fitted with the constant term held at exactly 1
+// (tools/fit_poly.py sin_tire: 2.1e-7 absolute / 2.6e-7 relative on the
+// range, the sin_pi_x2 level) -- two FFMA2 (four FMA-pipe cycles) fewer.
+// SHORT = false is sin_pi_x2 (|x| <= pi, C <= 2).
+template <bool SHORT>
+__device__ __forceinline__ float2 sin_tire_x2(float2 x) {
+  if (!SHORT) return sin_pi_x2(x);
+  const float2 t = __fmul2_rn(x, x);
+  float2 p = __ffma2_rn(t, bc2(-2.277197275e-08f), bc2(2.743227014e-06f));
+  p = __ffma2_rn(p, t, bc2(-1.983809780e-04f));
+  p = __ffma2_rn(p, t, bc2(8.333297446e-03f));
+  p = __ffma2_rn(p, t, bc2(-1.666666567e-01f));
+  p = __ffma2_rn(p, t, bc2(1.0f));
+  return __fmul2_rn(p, x);
+}
+
 // returns (sin x, cos x), any x: reduced to [-pi, pi] as in sincos_pi, but
 // unconditionally -- for |x| <= pi, n = 0 and x passes through unchanged --
 // so the particle step carries neither a compare nor predicated reduction

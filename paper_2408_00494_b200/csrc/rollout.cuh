@@ -376,7 +376,7 @@ __device__ __forceinline__ void particle_noise(const RollParams &P, int t, int k
 
 // One particle-step given its noise: re-project (or load the persistent
 // particle), Euler step, process noise.  Returns the post-step state in x.
-template <bool PERSIST, bool ZARR, int NK>
+template <bool PERSIST, bool ZARR, int NK, bool ST>
 __device__ __forceinline__ void particle_step(const RollParams &P, int t, int m, const float mean[8],
                                               const float L[10], const CtlDev &ctl, const StepShared &sh,
                                               float *cloud, const float z[7], float x[8]) {
@@ -396,8 +396,8 @@ __device__ __forceinline__ void particle_step(const RollParams &P, int t, int m,
   }
   // per-particle ok is discarded (belief.py:370); a re-projected particle
   // shares (vx, omega_f, omega_r, s) with the mean, hence the shared terms
-  if (PERSIST && t > 0) vehicle_step(x, ctl, P.V, P.tr);
-  else step_particle(x, sh, ctl, P.V, P.tr);
+  if (PERSIST && t > 0) vehicle_step<ST>(x, ctl, P.V, P.tr);
+  else step_particle<ST>(x, sh, ctl, P.V, P.tr);
   if (NK == NK_LAPLACE) {                // config-4 extension, after integration too
     x[0] += z[4];
     x[1] += z[5];
@@ -446,7 +446,7 @@ __device__ __forceinline__ void accumulate(float acc[18], const float x[8], cons
 // particle m + G are produced inside particle m's iteration, so the
 // quarter-rate IMAD.WIDE / MUFU work overlaps the FP32 dynamics in one
 // scheduling region; the last particle is peeled, so no draw is wasted.
-template <int G, bool PERSIST, bool ZARR, int NK>
+template <int G, bool PERSIST, bool ZARR, int NK, bool ST>
 __device__ __forceinline__ void particle_pass(const RollParams &P, int t, int k, int kg, int li,
                                               const float mean[8], const float L[10], const CtlDev &ctl,
                                               const StepShared &sh, float *cloud, float acc[18],
@@ -456,7 +456,7 @@ __device__ __forceinline__ void particle_pass(const RollParams &P, int t, int k,
   float x[8], zc[7], zn[7];
   particle_noise<ZARR, NK>(P, t, k, kg, li, zc);
   if (li + G < M) particle_noise<ZARR, NK>(P, t, k, kg, li + G, zn);
-  if (has0) particle_step<PERSIST, ZARR, NK>(P, t, li, mean, L, ctl, sh, cloud, zc, x);
+  if (has0) particle_step<PERSIST, ZARR, NK, ST>(P, t, li, mean, L, ctl, sh, cloud, zc, x);
 #pragma unroll
   for (int i = 0; i < 8; ++i) c[i] = __shfl_sync(0xffffffffu, x[i], 0, G);
   if (has0) accumulate<!PERSIST>(acc, x, c);
@@ -468,11 +468,11 @@ __device__ __forceinline__ void particle_pass(const RollParams &P, int t, int k,
 #pragma unroll
     for (int j = 0; j < 7; ++j) zc[j] = zn[j];
     particle_noise<ZARR, NK>(P, t, k, kg, m + G, zn);
-    particle_step<PERSIST, ZARR, NK>(P, t, m, mean, L, ctl, sh, cloud, zc, x);
+    particle_step<PERSIST, ZARR, NK, ST>(P, t, m, mean, L, ctl, sh, cloud, zc, x);
     accumulate<!PERSIST>(acc, x, c);
   }
   if (m < M) {                            // last particle: no look-ahead draw
-    particle_step<PERSIST, ZARR, NK>(P, t, m, mean, L, ctl, sh, cloud, zn, x);
+    particle_step<PERSIST, ZARR, NK, ST>(P, t, m, mean, L, ctl, sh, cloud, zn, x);
     accumulate<!PERSIST>(acc, x, c);
   }
 }
@@ -482,7 +482,7 @@ __device__ __forceinline__ void particle_pass(const RollParams &P, int t, int k,
 // ZARR: read the reference's normals instead of Philox; NK: the process
 // noise kind (NoiseKind), resolved once at kernel entry so every variant's
 // T loop holds exactly one particle loop (register allocation per variant).
-template <int G, bool PERSIST, bool ZARR, int NK>
+template <int G, bool PERSIST, bool ZARR, int NK, bool ST>
 __device__ __forceinline__ void bss_rollout(const RollParams &P) {
   extern __shared__ float4 smem4[];
   float *smem = reinterpret_cast<float *>(smem4);
@@ -535,7 +535,7 @@ __device__ __forceinline__ void bss_rollout(const RollParams &P) {
 #pragma unroll
     for (int i = 0; i < 18; ++i) acc[i] = 0.f;
     float c[8];
-    particle_pass<G, PERSIST, ZARR, NK>(P, t, k, kg, li, mean, L, ctl, sh, cloud, acc, c);
+    particle_pass<G, PERSIST, ZARR, NK, ST>(P, t, k, kg, li, mean, L, ctl, sh, cloud, acc, c);
     group_allreduce18<G>(acc, li, slots + (t & 1) * kSlotFloats);
 
     // moments (belief.py:275-308 semantics)
@@ -596,17 +596,25 @@ __device__ __forceinline__ void bss_rollout(const RollParams &P) {
 #else
 #define BSS_ROLLOUT_BOUNDS __launch_bounds__(kBlockThreads, BSS_MIN_BLOCKS)
 #endif
+// Kernel-entry dispatch on the launch-constant noise kind and tire-sine
+// range: every variant's T loop holds exactly one particle loop.
+template <int G, bool PERSIST, bool ZARR, bool ST>
+__device__ __forceinline__ void bss_rollout_nk(const RollParams &P) {
+  if (!ZARR && P.noise_kind == 1) bss_rollout<G, PERSIST, ZARR, NK_LAPLACE, ST>(P);
+  else if (P.noise_diag) bss_rollout<G, PERSIST, ZARR, NK_GAUSS_DIAG, ST>(P);
+  else bss_rollout<G, PERSIST, ZARR, NK_GAUSS_GENERAL, ST>(P);
+}
+
 template <int G, bool PERSIST, bool ZARR>
 __global__ void BSS_ROLLOUT_BOUNDS bss_rollout_kernel(const RollParams P) {
-  if (!ZARR && P.noise_kind == 1) bss_rollout<G, PERSIST, ZARR, NK_LAPLACE>(P);
-  else if (P.noise_diag) bss_rollout<G, PERSIST, ZARR, NK_GAUSS_DIAG>(P);
-  else bss_rollout<G, PERSIST, ZARR, NK_GAUSS_GENERAL>(P);
+  if (P.V.tire_short) bss_rollout_nk<G, PERSIST, ZARR, true>(P);
+  else bss_rollout_nk<G, PERSIST, ZARR, false>(P);
 }
 
 // Deterministic rollouts for kind "mppi" / "smppi" (controllers.py:320-338):
 // one lane per k, state carried in registers.
-template <bool SHIELD>
-__global__ void __launch_bounds__(kBlockThreads) det_rollout_kernel(const RollParams P) {
+template <bool SHIELD, bool ST>
+__device__ __forceinline__ void det_rollout(const RollParams &P) {
   const int kraw = blockIdx.x * kBlockThreads + threadIdx.x;
   if (kraw >= P.k_count) return;
   const int k = kraw, kg = P.k_begin + k;
@@ -629,7 +637,7 @@ __global__ void __launch_bounds__(kBlockThreads) det_rollout_kernel(const RollPa
       if (SHIELD && t > 0) total += shield_penalty(ho_cur, ho_prev, P);
     }
     const float4 cv = ctl_row[t];
-    const bool ok = vehicle_step(x, CtlDev{cv.x, cv.y, cv.z, cv.w}, P.V, P.tr);
+    const bool ok = vehicle_step<ST>(x, CtlDev{cv.x, cv.y, cv.z, cv.w}, P.V, P.tr);
     dead |= !ok;
     if (SHIELD) {
       h_prev = h_cur;
@@ -649,15 +657,22 @@ __global__ void __launch_bounds__(kBlockThreads) det_rollout_kernel(const RollPa
   P.cost_out[k] = dead ? __int_as_float(0x7f800000) : total;
 }
 
+template <bool SHIELD>
+__global__ void __launch_bounds__(kBlockThreads) det_rollout_kernel(const RollParams P) {
+  if (P.V.tire_short) det_rollout<SHIELD, true>(P);
+  else det_rollout<SHIELD, false>(P);
+}
+
 // step_array (dynamics.py:550-573): one particle per thread, FP64 I/O.
-__global__ void step_array_kernel(VehDev V, TrackDev tr, int n, const double *x, const double *u,
-                                  const double *w, double *xo, uint8_t *oko) {
+template <bool ST>
+__device__ __forceinline__ void step_array(const VehDev &V, const TrackDev &tr, int n, const double *x,
+                                           const double *u, const double *w, double *xo, uint8_t *oko) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   float s[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) s[j] = (float)x[(size_t)i * 8 + j];
-  const bool ok = vehicle_step(s, make_ctl((float)u[2 * (size_t)i], (float)u[2 * (size_t)i + 1], V), V, tr);
+  const bool ok = vehicle_step<ST>(s, make_ctl((float)u[2 * (size_t)i], (float)u[2 * (size_t)i + 1], V), V, tr);
   if (w != nullptr) {
 #pragma unroll
     for (int j = 0; j < 3; ++j) s[j] += (float)w[(size_t)i * 3 + j];
@@ -665,6 +680,12 @@ __global__ void step_array_kernel(VehDev V, TrackDev tr, int n, const double *x,
 #pragma unroll
   for (int j = 0; j < 8; ++j) xo[(size_t)i * 8 + j] = (double)s[j];
   oko[i] = ok ? 1 : 0;
+}
+
+__global__ void step_array_kernel(VehDev V, TrackDev tr, int n, const double *x, const double *u,
+                                  const double *w, double *xo, uint8_t *oko) {
+  if (V.tire_short) step_array<true>(V, tr, n, x, u, w, xo, oko);
+  else step_array<false>(V, tr, n, x, u, w, xo, oko);
 }
 
 }  // namespace bss

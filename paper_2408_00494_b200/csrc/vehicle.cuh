@@ -43,6 +43,7 @@ struct VehDev {
   float2 nBy;      // (-Byf, -Byr): the lateral-slip pair as one FFMA2 on (atan2 f, atan2 r)
   float dt_lf_iz, ndt_lr_iz;   // dt lf / Iz, -dt lr / Iz: the yaw-rate Euler update
   float dt_m;                  // dt / m: the (vx, vy) Euler update
+  int tire_short;              // max lateral C pi / 2 <= 2.2: kernels run step_particle<true>
 };
 
 // node[j] = {s_j, kappa_j, slope_j, s_{j+1}} plus a sentinel node[n].
@@ -284,6 +285,7 @@ __device__ __forceinline__ StepShared step_shared(const float x[8], const CtlDev
 // and finite).
 #ifdef BSS_EXACT_MATH
 // libdevice reference form (A/B parity builds, build_cuda(exact=True)).
+template <bool ST = false>
 __device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, const CtlDev &c,
                                               const VehDev &V, const TrackDev &tr) {
   const float vx = x[0], vy = x[1], r = x[2], ep = x[5], ey = x[6], s = x[7];
@@ -326,6 +328,8 @@ __device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, c
 // and the (vx, vy) / (e_psi, e_y) Euler updates run as FP32x2 lanes, one
 // issue slot per pair.  Every lane is an IEEE FMA/MUL/ADD, so all kernels
 // (which share this function) stay bit-identical to one another.
+// ST: short tire sine (sin_tire_x2<true>, lateral C <= 1.40; VehDev::tire_short).
+template <bool ST = false>
 __device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, const CtlDev &c,
                                               const VehDev &V, const TrackDev &tr) {
   const float vx = x[0], vy = x[1], r = x[2], ep = x[5], ey = x[6], s = x[7];
@@ -337,7 +341,7 @@ __device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, c
   // delta - A.x, alpha_r = -A.y
   const float2 ty = __fmul2_rn(V.Cy, atan_x2(make_float2(fmaf(V.nBy.x, A.x, h.byd.x), V.nBy.y * A.y)));
   // |ty| < C pi / 2 <= pi (lateral C <= 2, checked at context creation)
-  const float2 fy = __fmul2_rn(__fmul2_rn(V.Dy, sin_pi_x2(ty)), h.cx);
+  const float2 fy = __fmul2_rn(__fmul2_rn(V.Dy, sin_tire_x2<ST>(ty)), h.cx);
   // body-frame front force + rear longitudinal: (fxf cd - fyf sd + fxr, fxf sd + fyf cd)
   const float2 fb = __ffma2_rn(bc2(fy.x), h.nsd_cd, h.fb0);
   float frame = 1.f - h.kap * ey;
@@ -372,10 +376,11 @@ __device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, c
 }
 #endif
 
+template <bool ST = false>
 __device__ __forceinline__ bool vehicle_step(float x[8], const CtlDev &c, const VehDev &V,
                                              const TrackDev &tr) {
   const StepShared h = step_shared(x, c, V, tr);
-  return step_particle(x, h, c, V, tr);
+  return step_particle<ST>(x, h, c, V, tr);
 }
 
 __device__ __forceinline__ CtlDev make_ctl(float delta, float throttle, const VehDev &V) {

@@ -128,6 +128,20 @@ def check_atan(coef):
 
 def main():
     what = sys.argv[1] if len(sys.argv) > 1 else "atan"
+    if what == "sin_tire":
+        # sin x = x (1 + t Q(t)) on |x| <= 2.2 with Q of degree 4 (constant term of
+        # the bracket held at 1): the short lateral tire sine (fastmath.cuh sin_tire_x2)
+        xs = np.linspace(1e-5, 2.2, 40001)
+        t = xs * xs
+        g = (np.sin(xs) / xs - 1.0) / t
+        basis = np.stack([t ** k for k in range(4, -1, -1)], 1)
+        c = np.append(f32(lawson(basis, g, t / (np.sin(xs) / xs))), 1.0)
+        x32 = f32(xs)
+        y = f32(horner32(c, f32(x32 * x32)) * x32)
+        e = np.abs(y - np.sin(x32))
+        print(f"sin_tire: max abs err {e.max():.3e}, rel {(e / np.abs(np.sin(x32))).max():.3e}")
+        print("  coefficients (highest first):", ", ".join(f"{v:.9e}f" for v in c))
+        return
     if what == "atan_rat":
         p, q = fit_atan_rat()
         x = f32(np.concatenate([np.linspace(-40, 40, 2000001), np.geomspace(1e-6, 1e6, 400001)]))
