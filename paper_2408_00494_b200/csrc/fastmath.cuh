@@ -144,9 +144,11 @@ __device__ __forceinline__ float2 sin_tire_x2(float2 x) {
 // instructions (A/B: 4 straight-line instructions beat the guarded form)
 __device__ __forceinline__ float2 sincos_pi_x2(float x) {
   {
+    // one-constant Cody-Waite: exact for |x| <= pi (n = 0); beyond, the
+    // reduced angle carries n * 1.7e-7 of 2 pi's float rounding (a heading
+    // error past +-pi: reverse driving or a spun-out particle)
     const float n = rintf(x * 0.159154943f);
     x = fmaf(-n, 6.28318548e+00f, x);
-    x = fmaf(n, 1.74845553e-07f, x);
   }
   const float t = x * x;
   float2 p = kSinCosPi[0];

@@ -214,6 +214,7 @@ struct StepShared {
                               //   parts of the body-frame force sums
   float2 nsd_cd;              // (-sin delta, cos delta)
   float2 rev;                 // atan2 quadrant fold: (1, 0) for vx_eff > 0, (-1, pi) below
+  float2 dycx;                // (Dyf |cos|_f, Dyr |cos|_r): lateral peak x friction ellipse
   float2 byd;                 // (Byf delta, 0): front slip-angle offset of the lateral pair
 };
 
@@ -260,6 +261,7 @@ __device__ __forceinline__ StepShared step_shared(const float x[8], const CtlDev
   h.fb0 = make_float2(fmaf(h.fxf, c.cd, h.fxr), h.fxf * c.sd);
   h.nsd_cd = make_float2(-c.sd, c.cd);
   h.rev = (h.vxe >= 0.f) ? make_float2(1.f, 0.f) : make_float2(-1.f, 3.14159265358979f);
+  h.dycx = __fmul2_rn(V.Dy, h.cx);
   h.byd = make_float2(V.Byf * c.delta, 0.f);
   // _derivs_row wheel torque balance; rolling resistance opposes the spin
 #ifdef BSS_EXACT_MATH
@@ -335,13 +337,16 @@ __device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, c
   const float vx = x[0], vy = x[1], r = x[2], ep = x[5], ey = x[6], s = x[7];
   // slip-angle numerators (vy + lf r, vy - lr r); atan2(., vxe) = atan(. / vxe)
   // for vxe > 0, +-pi shifted for vxe < 0 (vxe is shared by the rollout)
+  // (Y: its IEEE sign, signed zeros included, picks atan2's +-pi when
+  // vx_eff < 0, as in the reference; folding 1/vx_eff into the FFMA2 would
+  // lose it)
   const float2 Y = __ffma2_rn(bc2(r), V.lf_nlr, bc2(vy));
   const float2 A = atan2_x2(__fmul2_rn(Y, bc2(h.rx)), Y, h.rev);
   // (B_f alpha_f, B_r alpha_r) = (Byf delta - Byf A.x, -Byr A.y): alpha_f =
   // delta - A.x, alpha_r = -A.y
   const float2 ty = __fmul2_rn(V.Cy, atan_x2(make_float2(fmaf(V.nBy.x, A.x, h.byd.x), V.nBy.y * A.y)));
   // |ty| < C pi / 2 <= pi (lateral C <= 2, checked at context creation)
-  const float2 fy = __fmul2_rn(__fmul2_rn(V.Dy, sin_tire_x2<ST>(ty)), h.cx);
+  const float2 fy = __fmul2_rn(h.dycx, sin_tire_x2<ST>(ty));
   // body-frame front force + rear longitudinal: (fxf cd - fyf sd + fxr, fxf sd + fyf cd)
   const float2 fb = __ffma2_rn(bc2(fy.x), h.nsd_cd, h.fb0);
   float frame = 1.f - h.kap * ey;

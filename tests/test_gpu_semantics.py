@@ -129,6 +129,35 @@ def test_step_array_matches_oracle(oval, model):
     dc.close()
 
 
+def test_step_array_reverse_zero_slip(oval, model):
+    """Reverse driving with zero lateral velocity and yaw rate: both slip
+    angles are atan2(+0, vx < 0) = +pi in the reference (dynamics.py:381-382),
+    so the device must keep the IEEE sign of vy + l r (signed zeros
+    included) rather than derive it from the product with 1/vx."""
+    n = 4
+    x = np.zeros((n, 8))
+    x[:, 0] = [-2.0, -0.8, -3.5, -2.0]
+    x[:, 3] = x[:, 0] / 0.095
+    x[:, 4] = x[:, 0] / 0.095
+    x[:, 6] = [0.2, -0.1, 0.0, 0.3]
+    x[:, 7] = [20.0, 5.0, 40.0, 1.0]
+    x[3, 1] = 1e-3                      # one non-degenerate row
+    u = np.tile([0.05, -0.5], (n, 1))
+    ctx = mc.RolloutContext(model, oval, mc.CostSpec())
+    prob, keep = mc.build_problem("mppi", 1, 1, 1, 1.0, 0.0, np.eye(2), None, mc.ControlBounds(),
+                                  False, ctx)
+    dc = mc.DeviceContext(prob)
+    out = np.empty_like(x)
+    ok = np.empty(n, dtype=np.uint8)
+    _lib.check(dc.lib.bssmppi_step_array(dc.h, n, _lib.dptr(x), _lib.dptr(u), None, _lib.dptr(out),
+                                         ok.ctypes.data_as(_lib.C.POINTER(_lib.C.c_uint8))))
+    dc.close()
+    ref, ref_ok = orc.step_euler(x, u, orc.phys(model), oval, model.dt)
+    assert np.array_equal(ok.astype(bool), ref_ok)
+    scale = np.array([5, 1, 1, 50, 50, 1, 1, oval.length])
+    assert (np.abs(out - ref) / scale).max() < 2e-6
+
+
 def _f32_track_s(s, L, closed):
     """float32 emulation of the device arc-length wrap (vehicle.cuh track_s:
     Python floor-mod on a closed track, exact on [-L, 2L) and fmodf beyond;
