@@ -96,16 +96,6 @@ __device__ __forceinline__ float2 atan2_x2(float2 x, float2 Y, float2 rev) {
   return make_float2(copysignf(mag.x, Y.x), copysignf(mag.y, Y.y));
 }
 
-// sin and cos of one argument in one packed Horner chain: lane x runs the
-// sine polynomial (padded with a leading 0, so it is evaluated exactly as
-// the scalar Horner), lane y the cosine; coefficients as in sincos_pi.
-__constant__ float2 kSinCosPi[9] = {
-    {0.0f, 4.101670311e-14f},           {-6.416872784e-13f, -1.134152147e-11f},
-    {1.582333015e-10f, 2.086320672e-09f}, {-2.502759777e-08f, -2.755647870e-07f},
-    {2.755584774e-06f, 2.480155672e-05f}, {-1.984121918e-04f, -1.388888806e-03f},
-    {8.333332837e-03f, 4.166666791e-02f}, {-1.666666716e-01f, -5.0e-01f},
-    {1.0f, 1.0f}};
-
 // sin of two arguments in [-pi, pi] (the sincos_pi sine polynomial, packed;
 // ~1 ulp, relative accuracy kept near 0 unlike MUFU.SIN's absolute 2^-21.4).
 __device__ __forceinline__ float2 sin_pi_x2(float2 x) {
@@ -138,10 +128,22 @@ __device__ __forceinline__ float2 sin_tire_x2(float2 x) {
   return __fmul2_rn(p, x);
 }
 
-// returns (sin x, cos x), any x: reduced to [-pi, pi] as in sincos_pi, but
-// unconditionally -- for |x| <= pi, n = 0 and x passes through unchanged --
-// so the particle step carries neither a compare nor predicated reduction
-// instructions (A/B: 4 straight-line instructions beat the guarded form)
+// (sin, cos) on [0, pi/2] in one packed Horner chain: lane x the sine
+// x S(t) (degree 4 in t = x^2, padded with a leading 0), lane y the cosine
+// C(t) (degree 5); tools/fit_poly.py sincos_half: 1.2e-7 / 1.0e-7 absolute,
+// ~1e-7 relative for the sine near 0.
+__constant__ float2 kSinCosHalf[6] = {
+    {0.0f, -2.604962503e-07f},            {2.605039072e-06f, 2.476005830e-05f},
+    {-1.980899542e-04f, -1.388835954e-03f}, {8.333049715e-03f, 4.166663438e-02f},
+    {-1.666665822e-01f, -5.0e-01f},         {1.0f, 1.0f}};
+
+// returns (sin x, cos x), any x.  Reduced to [-pi, pi] unconditionally
+// (for |x| <= pi, n = 0 and x passes through unchanged -- no compare, no
+// predicated block), then reflected to h = min(|x|, pi - |x|) in [0, pi/2]:
+// sin x = sign(x) sin h, cos x = +-cos h.  The half range halves the
+// polynomial: 5 FFMA2 instead of 8 for one FADD and three ALU operations
+// (min, copysign, select), i.e. 5 FMA-pipe cycles fewer.  For |x| <= pi/2,
+// h = |x| exactly; past it pi - |x| carries pi_f32's 8.7e-8 offset.
 __device__ __forceinline__ float2 sincos_pi_x2(float x) {
   {
     // one-constant Cody-Waite: exact for |x| <= pi (n = 0); beyond, the
@@ -150,11 +152,13 @@ __device__ __forceinline__ float2 sincos_pi_x2(float x) {
     const float n = rintf(x * 0.159154943f);
     x = fmaf(-n, 6.28318548e+00f, x);
   }
-  const float t = x * x;
-  float2 p = kSinCosPi[0];
+  const float a = fabsf(x), b = 3.14159265f - a;
+  const float h = fminf(a, b);
+  const float t = h * h;
+  float2 p = kSinCosHalf[0];
 #pragma unroll
-  for (int j = 1; j < 9; ++j) p = __ffma2_rn(p, bc2(t), kSinCosPi[j]);
-  return make_float2(p.x * x, p.y);
+  for (int j = 1; j < 6; ++j) p = __ffma2_rn(p, bc2(t), kSinCosHalf[j]);
+  return make_float2(copysignf(p.x * h, x), b < a ? -p.y : p.y);
 }
 
 // atan2(y, x) given r = 1/x (x != 0, already computed by the caller):

@@ -113,19 +113,37 @@ def test_atan_x2():
     assert np.all(np.sign(y) == np.sign(x))
 
 
-def test_sincos_pi_x2_table_is_the_scalar_polynomials():
-    """The packed (sin, cos) Horner table holds exactly the scalar
-    sincos_pi coefficients (sine padded with a leading 0, which the FMA
-    passes through exactly), so both forms round identically."""
-    body = SRC[SRC.index("kSinCosPi[9] = {"):]
+def test_sincos_pi_x2_half_range():
+    """Packed heading / centerline (sin, cos): unconditional one-constant
+    reduction, reflection to h = min(|x|, pi - |x|), the kSinCosHalf Horner
+    chain (sine padded with a leading 0) -- emulated in float32 in the
+    kernel's order on [-pi, pi] and beyond."""
+    body = SRC[SRC.index("kSinCosHalf[6] = {"):]
     body = body[:body.index("};")]
     pairs = re.findall(r"\{([-0-9.e+]+)f, ([-0-9.e+]+)f\}", body)
-    assert len(pairs) == 9
+    assert len(pairs) == 6
     sin_c = [np.float32(float(a)) for a, _ in pairs]
     cos_c = [np.float32(float(b)) for _, b in pairs]
-    assert sin_c[0] == 0.0
-    assert sin_c[1:] == _coeffs("void sincos_pi")
-    assert cos_c == _coeffs("void sincos_pi", "q")
+    assert sin_c[0] == 0.0 and sin_c[-1] == 1.0 and cos_c[-1] == 1.0
+    f = np.float32
+    x = np.concatenate([np.linspace(-np.pi, np.pi, 400001), np.linspace(-9.0, 9.0, 100001)]).astype(f)
+    n = np.rint((x * f(0.159154943)).astype(f)).astype(f)
+    xr = (x.astype(np.float64) - n.astype(np.float64) * np.float64(f(6.28318548))).astype(f)
+    a = np.abs(xr)
+    b = (f(3.14159265) - a).astype(f)
+    h = np.minimum(a, b)
+    t = (h * h).astype(f)
+    ps, pc = _horner(sin_c, t), _horner(cos_c, t)
+    s_dev = np.copysign((ps * h).astype(f), xr).astype(np.float64)
+    c_dev = np.where(b < a, -pc, pc).astype(np.float64)
+    x64 = x.astype(np.float64)
+    es, ec = np.abs(s_dev - np.sin(x64)), np.abs(c_dev - np.cos(x64))
+    inside = np.abs(x64) <= np.pi
+    assert es[inside].max() < 2.5e-7 and ec[inside].max() < 2.5e-7, (es[inside].max(), ec[inside].max())
+    assert es.max() < 2e-6 and ec.max() < 2e-6          # reduced: + n * 1.7e-7 of 2 pi_f32
+    small = np.abs(x64) < 0.7                          # heading errors: relative accuracy near 0
+    nz = small & (np.abs(x64) > 1e-3)
+    assert (es[nz] / np.abs(np.sin(x64[nz]))).max() < 3e-7
 
 
 def test_centred_uniform2_is_exact():

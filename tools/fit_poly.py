@@ -128,6 +128,15 @@ def check_atan(coef):
 
 def main():
     what = sys.argv[1] if len(sys.argv) > 1 else "atan"
+    if what == "sincos_half":
+        # (sin, cos) on [0, pi/2]: sin = x S(t) (degree 4), cos = C(t) (degree 5)
+        xs = np.linspace(1e-5, np.pi / 2 + 1e-3, 40001)
+        t = xs * xs
+        for name, g, deg in (("sin", np.sin(xs) / xs, 4), ("cos", np.cos(xs), 5)):
+            basis = np.stack([t ** k for k in range(deg, -1, -1)], 1)
+            c = f32(lawson(basis, g, np.ones_like(g)))
+            print(f"{name}:", ", ".join(f"{v:.9e}f" for v in c))
+        return
     if what == "sin_tire":
         # sin x = x (1 + t Q(t)) on |x| <= 2.2 with Q of degree 4 (constant term of
         # the bracket held at 1): the short lateral tire sine (fastmath.cuh sin_tire_x2)
