@@ -25,7 +25,11 @@
 //   * everything per (k, t) -- stage cost, shared step terms, Cholesky,
 //     DCBF, penalty, frame check -- is computed redundantly by the G lanes
 //     (same issue slots as one lane); the controls, their clamp and the
-//     control cost are sampled once per (k, t) in the prologue.
+//     control cost are sampled once per (k, t) in the prologue;
+//   * launch constants (process-noise kind, tire-sine range) are resolved
+//     once at kernel entry, so each variant's T loop holds one branch-free
+//     particle loop; the FMA pipe (shared by the Philox IMAD.WIDE, FFMA2 and
+//     FFMA: 4 / 2 / 1 cycles) is the budget the particle step is written to.
 #pragma once
 #include <cstdint>
 

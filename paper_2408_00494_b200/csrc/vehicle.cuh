@@ -352,12 +352,7 @@ __device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, c
   float frame = 1.f - h.kap * ey;
   bool ok = frame > 0.f;
   if (frame < 1e-3f) frame = 1e-3f;
-#ifdef BSS_MUFU_HEADING
-  float2 sc;
-  __sincosf(ep, &sc.x, &sc.y);
-#else
   const float2 sc = sincos_pi_x2(ep);          // (sin e_psi, cos e_psi)
-#endif
   const float2 vsc = __fmul2_rn(bc2(vy), sc);  // (vy se, vy ce)
   // frame in [1e-3, 1 + kappa w]: MUFU.RCP without __fdividef's huge-divisor guard
   const float ds = fmaf(vx, sc.y, -vsc.x) * rcp_approx(frame);
