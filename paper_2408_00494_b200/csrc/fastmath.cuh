@@ -53,47 +53,44 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return y;
 }
 
-// atan of two arguments: a = min(|x|, 1/|x|) in [0, 1], atan(a) = a + a s P(s)
-// with s = a^2 (degree-6 minimax in s, tools/fit_poly.py atan: 3.0 ulp /
-// 1.8e-7 absolute on the whole line; degree 7 was 1.9 ulp at 1.2% more
-// time and the same parity), pi/2 - atan(a) for |x| > 1, sign of x.
-__device__ __forceinline__ float2 atan_x2(float2 x) {
+// atan of two arguments: a = min(|x|, 1/|x|) in [0, 1], atan(a) = a Q(s),
+// Q = 1 + s P(s), s = a^2 (P degree-6 minimax, tools/fit_poly.py atan), and
+// pi/2 - atan(a) for |x| > 1 -- folded into the final FFMA2 as
+// fma(+-a, Q, 0 or pi/2) with per-lane sign/offset selects (ALU), which
+// saves the separate multiply and subtraction (2 FMA-pipe cycles per pair;
+// 3.3 ulp / 2.0e-7 absolute on the whole line, pinned in test_fastmath).
+// Returns |atan(x)| folded with rev = (r, o): r |atan x| + o for the caller's
+// quadrant shift; lanes select -a when (|x| > 1) != (r < 0) and offset
+// pi/2 when |x| > 1, else o.
+__device__ __forceinline__ float2 atan_mag_x2(float2 x, bool neg, float off) {
   const float tx = fabsf(x.x), ty = fabsf(x.y);
   const float2 a = make_float2(fminf(tx, rcp_approx(tx)), fminf(ty, rcp_approx(ty)));
   const float2 s = __fmul2_rn(a, a);
-  float2 p = __ffma2_rn(s, bc2(-4.822528455e-03f), bc2(2.473404258e-02f));
-  p = __ffma2_rn(p, s, bc2(-6.020310149e-02f));
-  p = __ffma2_rn(p, s, bc2(9.968471527e-02f));
-  p = __ffma2_rn(p, s, bc2(-1.404132694e-01f));
-  p = __ffma2_rn(p, s, bc2(1.997421384e-01f));
-  p = __ffma2_rn(p, s, bc2(-3.333239257e-01f));
-  p = __fmul2_rn(p, s);
-  p = __ffma2_rn(a, p, a);
-  const float2 q = __fadd2_rn(bc2(1.57079637f), make_float2(-p.x, -p.y));
-  return make_float2(copysignf(tx > 1.f ? q.x : p.x, x.x), copysignf(ty > 1.f ? q.y : p.y, x.y));
+  float2 q = __ffma2_rn(s, bc2(-4.822528455e-03f), bc2(2.473404258e-02f));
+  q = __ffma2_rn(q, s, bc2(-6.020310149e-02f));
+  q = __ffma2_rn(q, s, bc2(9.968471527e-02f));
+  q = __ffma2_rn(q, s, bc2(-1.404132694e-01f));
+  q = __ffma2_rn(q, s, bc2(1.997421384e-01f));
+  q = __ffma2_rn(q, s, bc2(-3.333239257e-01f));
+  q = __ffma2_rn(q, s, bc2(1.0f));
+  const bool bx = tx > 1.f, by = ty > 1.f;
+  const float2 sa = make_float2((bx != neg) ? -a.x : a.x, (by != neg) ? -a.y : a.y);
+  return __ffma2_rn(sa, q, make_float2(bx ? 1.57079637f : off, by ? 1.57079637f : off));
+}
+
+__device__ __forceinline__ float2 atan_x2(float2 x) {
+  const float2 m = atan_mag_x2(x, false, 0.f);
+  return make_float2(copysignf(m.x, x.x), copysignf(m.y, x.y));
 }
 
 // atan2(Y, X) of two arguments given x = Y / X (via the caller's shared
 // reciprocal of X) and rev = (1, 0) for X > 0, (-1, pi) for X < 0:
-// sign(Y) (rev.y + rev.x atan|x|) -- the left-half-plane shift folded into
-// one FFMA2 (bit-identical to atan(x) + copysign(pi, Y) there, and to
-// atan(x) itself for X > 0).
+// sign(Y) (rev.y + rev.x atan|x|), the left-half-plane shift folded into the
+// same final FFMA2 (for X > 0 identical to atan_x2); the sign comes from Y
+// itself, so atan2(+-0, X < 0) = +-pi as in the reference.
 __device__ __forceinline__ float2 atan2_x2(float2 x, float2 Y, float2 rev) {
-  const float tx = fabsf(x.x), ty = fabsf(x.y);
-  const float2 a = make_float2(fminf(tx, rcp_approx(tx)), fminf(ty, rcp_approx(ty)));
-  const float2 s = __fmul2_rn(a, a);
-  float2 p = __ffma2_rn(s, bc2(-4.822528455e-03f), bc2(2.473404258e-02f));
-  p = __ffma2_rn(p, s, bc2(-6.020310149e-02f));
-  p = __ffma2_rn(p, s, bc2(9.968471527e-02f));
-  p = __ffma2_rn(p, s, bc2(-1.404132694e-01f));
-  p = __ffma2_rn(p, s, bc2(1.997421384e-01f));
-  p = __ffma2_rn(p, s, bc2(-3.333239257e-01f));
-  p = __fmul2_rn(p, s);
-  p = __ffma2_rn(a, p, a);
-  const float2 q = __fadd2_rn(bc2(1.57079637f), make_float2(-p.x, -p.y));
-  const float2 base = make_float2(tx > 1.f ? q.x : p.x, ty > 1.f ? q.y : p.y);
-  const float2 mag = __ffma2_rn(bc2(rev.x), base, bc2(rev.y));
-  return make_float2(copysignf(mag.x, Y.x), copysignf(mag.y, Y.y));
+  const float2 m = atan_mag_x2(x, rev.x < 0.f, rev.y);
+  return make_float2(copysignf(m.x, Y.x), copysignf(m.y, Y.y));
 }
 
 // sin of two arguments in [-pi, pi] (the sincos_pi sine polynomial, packed;

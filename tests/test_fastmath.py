@@ -86,16 +86,18 @@ def test_sin_tire_x2_short():
 
 
 def _atan_x2_coeffs():
-    body = SRC[SRC.index("float2 atan_x2"):]
+    body = SRC[SRC.index("float2 atan_mag_x2"):]
     body = body[:body.index("\n}\n")]
     first = re.findall(r"bc2\(([-0-9.e+]+)f\)", body)
+    assert [float(v) for v in first[7:]] == [1.0]   # Q = 1 + s P(s): the Horner ends on 1
     return [np.float32(float(v)) for v in first[:7]]
 
 
 def test_atan_x2():
     """Packed arctangent (slip angles and both magic formulas): the device
-    algorithm in float32 with the kernel's Horner order, <= 3.1 ulp /
-    1.85e-7 absolute on the whole line (libdevice atanf: 2 ulp)."""
+    algorithm in float32 with the kernel's Horner order and folded final
+    FFMA, <= 3.3 ulp / 2.0e-7 absolute on the whole line (libdevice atanf:
+    2 ulp)."""
     import sys
     sys.path.insert(0, str(Path(__file__).resolve().parent.parent / "tools"))
     from fit_poly import atan32
@@ -107,9 +109,9 @@ def test_atan_x2():
     y = atan32(c, x)
     ex = np.arctan(x)
     e = np.abs(y - ex)
-    assert e.max() < 1.85e-7, e.max()
+    assert e.max() < 2.0e-7, e.max()
     ulp = np.spacing(np.abs(ex).astype(np.float32)).astype(np.float64)
-    assert (e / ulp).max() <= 3.1
+    assert (e / ulp).max() <= 3.3
     assert np.all(np.sign(y) == np.sign(x))
 
 

@@ -59,18 +59,18 @@ def fit_atan(deg=7):
 
 
 def atan32(coef, x):
-    """Device algorithm: a = min(|x|, 1/|x|), p = a + a s P(s), pi/2 - p for
-    |x| > 1, sign of x.  MUFU.RCP is modelled as a correctly rounded
+    """Device algorithm (fastmath.cuh atan_mag_x2): a = min(|x|, 1/|x|),
+    Q = 1 + s P(s) by Horner, r = fma(+-a, Q, 0 or pi/2) (pi/2 - a Q for
+    |x| > 1), sign of x.  MUFU.RCP is modelled as a correctly rounded
     reciprocal (the hardware's is within 1 ulp)."""
     t = np.abs(x)
     with np.errstate(divide="ignore"):
         r = f32(1.0 / t)
     a = np.minimum(t, r)
     s = f32(a * a)
-    p = horner32(coef, s)
-    p = f32(p * s)
-    p = fma32(a, p, a)
-    p = np.where(t > 1.0, f32(np.float32(1.57079637) - p), p)
+    q = horner32(np.append(coef, 1.0), s)
+    big = t > 1.0
+    p = fma32(np.where(big, -a, a), q, np.where(big, np.float64(np.float32(1.57079637)), 0.0))
     return np.copysign(p, x)
 
 
