@@ -522,6 +522,7 @@ __device__ __forceinline__ void bss_rollout(const RollParams &P) {
   float ho_prev = ho_cur;
   bool dead = false;
   const float4 *ctl_row = P.ctl + (size_t)k * P.T;
+  float kap_mean = curvature(P.tr, mean[7]);   // kappa(s_bar): frame check and next step's shared terms
 
   for (int t = 0; t < P.T; ++t) {
     total += stage_cost(mean, P);
@@ -533,7 +534,7 @@ __device__ __forceinline__ void bss_rollout(const RollParams &P) {
     const float4 cv = ctl_row[t];
     const CtlDev ctl{cv.x, cv.y, cv.z, cv.w};
     StepShared sh;
-    if (!(PERSIST && t > 0)) sh = step_shared(mean, ctl, P.V, P.tr);
+    if (!(PERSIST && t > 0)) sh = step_shared(mean, ctl, P.V, P.tr, kap_mean);
 
     float acc[18];
 #pragma unroll
@@ -567,8 +568,8 @@ __device__ __forceinline__ void bss_rollout(const RollParams &P) {
     }
     // ok = finite(mean) & finite(cov) & 1 - kappa(s_bar) e_bar > 0 (belief.py:376-379)
     const bool fin = all_finite8(mu) && all_finite8(C) && all_finite2(C[8], C[9]);
-    const float kap = curvature(P.tr, mu[7]);
-    const bool ok = fin && (1.f - kap * mu[6] > 0.f);
+    kap_mean = curvature(P.tr, mu[7]);
+    const bool ok = fin && (1.f - kap_mean * mu[6] > 0.f);
     dead |= !ok;
     // _finite_or_zero (controllers.py:231-235, 311-312)
 #pragma unroll
@@ -578,6 +579,7 @@ __device__ __forceinline__ void bss_rollout(const RollParams &P) {
       for (int i = 0; i < 8; ++i) mean[i] = isfinite(mu[i]) ? mu[i] : 0.f;
 #pragma unroll
       for (int i = 0; i < 10; ++i) C[i] = isfinite(C[i]) ? C[i] : 0.f;
+      kap_mean = curvature(P.tr, mean[7]);
     }
     h_prev = h_cur;
     h_cur = dcbf(mean[6], sigma_of(C[9]), P);

@@ -218,8 +218,10 @@ struct StepShared {
   float2 byd;                 // (Byf delta, 0): front slip-angle offset of the lateral pair
 };
 
+// kap: kappa(x[7]), supplied by the caller (the rollout already has it from
+// the belief mean's frame check).
 __device__ __forceinline__ StepShared step_shared(const float x[8], const CtlDev &c, const VehDev &V,
-                                                  const TrackDev &tr) {
+                                                  const TrackDev &tr, float kap) {
   const float vx = x[0], wf = x[3], wr = x[4], s = x[7];
   StepShared h;
   // _tire_row: low-speed floor keeps the sign of vx.
@@ -278,7 +280,7 @@ __device__ __forceinline__ StepShared step_shared(const float x[8], const CtlDev
     h.wf1 = isfinite(h.wf1) ? h.wf1 : 0.f;
     h.wr1 = isfinite(h.wr1) ? h.wr1 : 0.f;
   }
-  h.kap = curvature(tr, s);
+  h.kap = kap;
   return h;
 }
 
@@ -379,7 +381,7 @@ __device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, c
 template <bool ST = false>
 __device__ __forceinline__ bool vehicle_step(float x[8], const CtlDev &c, const VehDev &V,
                                              const TrackDev &tr) {
-  const StepShared h = step_shared(x, c, V, tr);
+  const StepShared h = step_shared(x, c, V, tr, curvature(tr, x[7]));
   return step_particle<ST>(x, h, c, V, tr);
 }
 
