@@ -523,6 +523,13 @@ __device__ __forceinline__ void bss_rollout(const RollParams &P) {
   bool dead = false;
   const float4 *ctl_row = P.ctl + (size_t)k * P.T;
   float kap_mean = curvature(P.tr, mean[7]);   // kappa(s_bar): frame check and next step's shared terms
+  // The step's control row and shared terms are produced at the end of the
+  // previous step (after its moments): the control-row load then overlaps
+  // the group reduction, and step_shared's dependency chain runs beside the
+  // Cholesky's instead of after it -- the per-step latency that bounds the
+  // small (few-rollouts-per-SM) shapes.
+  float4 cv = ctl_row[0];
+  StepShared sh = step_shared(mean, CtlDev{cv.x, cv.y, cv.z, cv.w}, P.V, P.tr, kap_mean);
 
   for (int t = 0; t < P.T; ++t) {
     total += stage_cost(mean, P);
@@ -531,16 +538,14 @@ __device__ __forceinline__ void bss_rollout(const RollParams &P) {
       if (inside) total += P.c_obs;
       if (t > 0) total += shield_penalty(ho_cur, ho_prev, P);
     }
-    const float4 cv = ctl_row[t];
     const CtlDev ctl{cv.x, cv.y, cv.z, cv.w};
-    StepShared sh;
-    if (!(PERSIST && t > 0)) sh = step_shared(mean, ctl, P.V, P.tr, kap_mean);
 
     float acc[18];
 #pragma unroll
     for (int i = 0; i < 18; ++i) acc[i] = 0.f;
     float c[8];
     particle_pass<G, PERSIST, ZARR, NK, ST>(P, t, k, kg, li, mean, L, ctl, sh, cloud, acc, c);
+    if (t + 1 < P.T) cv = ctl_row[t + 1];
     group_allreduce18<G>(acc, li, slots + (t & 1) * kSlotFloats);
 
     // moments (belief.py:275-308 semantics)
@@ -590,6 +595,7 @@ __device__ __forceinline__ void bss_rollout(const RollParams &P) {
     if (!PERSIST) {
       chol4(C, L, P.chol_rank);
       if (!ZARR) scale_raw(L);
+      sh = step_shared(mean, CtlDev{cv.x, cv.y, cv.z, cv.w}, P.V, P.tr, kap_mean);
     }
   }
   total += P.term * stage_cost(mean, P) + shield_penalty(h_cur, h_prev, P);
