@@ -332,6 +332,14 @@ int launch_rollout(bssmppi_ctx *c, const RollParams &rp, bool zarr) {
 // rank record into rec_out (final = 0) or the final v+ (final = 1).
 int launch_update(bssmppi_ctx *c, bool final_, double *rec_out) {
   const int T2 = 2 * c->T;
+  if (final_ && c->k_count <= kSmallK && T2 <= kCombinePart) {   // one launch at small K
+    update_small_kernel<<<1, kCombThreads, 0, c->stream>>>(c->k_count, c->k_begin, T2, c->d_cost, c->d_u, c->lam,
+                                                           c->lo[0], c->lo[1], c->hi[0], c->hi[1], c->d_out,
+                                                           c->d_state + 24, c->d_out + T2);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(BSSMPPI_ERR_CUDA, "update launch: %s", cudaGetErrorString(e));
+    return BSSMPPI_OK;
+  }
   update_partials_kernel<float, float><<<c->nblocks, kUpdThreads, 0, c->stream>>>(
       c->k_count, c->k_begin, T2, c->d_cost, c->d_u, c->lam, c->chunk, c->d_rec);
   combine_kernel<<<1, kCombThreads, 0, c->stream>>>(

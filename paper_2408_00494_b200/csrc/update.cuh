@@ -212,4 +212,99 @@ combine_kernel(int nrec, int T2, const double *rec, double lam, int final_, doub
   }
 }
 
+// Small-K update in ONE launch (K <= kSmallK, single context, final v+):
+// the same weights, sums and outputs as update_partials_kernel +
+// combine_kernel(final = 1) with one record, without the second launch and
+// the record round trip -- the update is latency-bound at small K (C1, C2,
+// closed-loop control).  Fixed-order reductions (deterministic).
+constexpr int kSmallK = 1024;   // at K = 2048 the two-level update was already faster (A/B)
+
+__global__ void __launch_bounds__(kCombThreads)
+update_small_kernel(int n, int k_begin, int T2, const float *costs, const float *u, double lam, double lo0,
+                    double lo1, double hi0, double hi1, double *vplus, float *plan_out, double *head_out) {
+  __shared__ double s_w[kSmallK];
+  __shared__ double s_part[kCombinePart];   // also the reduction scratch of steps 1-2
+  __shared__ double s_head[kRecHead];
+  static_assert(4 * kCombThreads <= kCombinePart, "reduction scratch must fit s_part");
+  double *s_a = s_part, *s_b = s_part + kCombThreads, *s_c = s_part + 2 * kCombThreads;
+  long long *s_i = reinterpret_cast<long long *>(s_part + 3 * kCombThreads);
+  const int tid = threadIdx.x;
+  const double INF = __longlong_as_double(0x7ff0000000000000ll);
+  // 1. minimum over finite costs (ties -> smallest k), finite count
+  double mn = INF, cnt = 0.0;
+  long long arg = -1;
+  for (int k = tid; k < n; k += kCombThreads) {
+    const double c = (double)costs[k];
+    if (isfinite(c)) {
+      cnt += 1.0;
+      if (c < mn) { mn = c; arg = k; }
+    }
+  }
+  s_a[tid] = mn; s_i[tid] = arg; s_c[tid] = cnt;
+  __syncthreads();
+  for (int s = kCombThreads / 2; s > 0; s >>= 1) {
+    if (tid < s) {
+      const double a = s_a[tid], b = s_a[tid + s];
+      const long long ia = s_i[tid], ib = s_i[tid + s];
+      if (b < a || (b == a && ib >= 0 && (ia < 0 || ib < ia))) { s_a[tid] = b; s_i[tid] = ib; }
+      s_c[tid] += s_c[tid + s];
+    }
+    __syncthreads();
+  }
+  const double beta = s_a[0];
+  const long long argmin = s_i[0];
+  const double nfin = s_c[0];
+  __syncthreads();
+  // 2. weights w_k = exp(-(S_k - beta) / lambda) (controllers.py:180-187); Z, Z2
+  double z = 0.0, z2 = 0.0;
+  for (int k = tid; k < n; k += kCombThreads) {
+    const double c = (double)costs[k];
+    const double w = (nfin > 0.0 && isfinite(c)) ? exp(-(c - beta) / lam) : 0.0;
+    s_w[k] = w;
+    z += w;
+    z2 += w * w;
+  }
+  s_a[tid] = z; s_b[tid] = z2;
+  __syncthreads();
+  for (int s = kCombThreads / 2; s > 0; s >>= 1) {
+    if (tid < s) { s_a[tid] += s_a[tid + s]; s_b[tid] += s_b[tid + s]; }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    s_head[0] = beta; s_head[1] = s_a[0]; s_head[2] = s_b[0]; s_head[3] = nfin;
+    s_head[4] = (double)(argmin < 0 ? -1 : argmin + k_begin);
+  }
+  __syncthreads();
+  // 3. N[col] = sum_k w_k u_k[col] (controllers.py:190-194): (column,
+  //    k-slice) items over all threads, slice partials summed in slice order
+  const int ns = max(1, min(kCombineSlices, min(kCombinePart / T2, n)));
+  const int per = (n + ns - 1) / ns;
+  for (int it = tid; it < ns * T2; it += kCombThreads) {
+    const int col = it % T2, sl = it / T2;
+    const int k0 = sl * per, k1 = min(n, k0 + per);
+    const float *src = u + col;
+    double a = 0.0;
+#pragma unroll 16
+    for (int k = k0; k < k1; ++k) a = fma(s_w[k], (double)src[(size_t)k * T2], a);
+    s_part[it] = a;
+  }
+  __syncthreads();
+  // 4. v+ = clip(N / Z); head; warm-start shifted plan (controllers.py:154-156)
+  for (int col = tid; col < T2; col += kCombThreads) {
+    double a = 0.0;
+    for (int sl = 0; sl < ns; ++sl) a += s_part[sl * T2 + col];
+    const double v = a / s_head[1];
+    const double l = (col & 1) ? lo1 : lo0, h = (col & 1) ? hi1 : hi0;
+    vplus[col] = fmin(fmax(v, l), h);
+  }
+  if (tid < kRecHead) head_out[tid] = s_head[tid];
+  if (plan_out != nullptr) {
+    __syncthreads();
+    for (int col = tid; col < T2; col += kCombThreads) {
+      const int src = (col + 2 < T2) ? col + 2 : col;   // drop first, repeat last
+      plan_out[col] = (float)vplus[src];
+    }
+  }
+}
+
 }  // namespace bss
