@@ -74,7 +74,8 @@ struct bssmppi_ctx {
   int nblocks = 0, chunk = 0;
   double *d_out = nullptr;    // vplus[2T] | head[5]
   float *h_state = nullptr;   // pinned
-  double *h_out = nullptr;    // pinned
+  double *h_out = nullptr;    // pinned, mapped: final update kernels write v+ and head here
+  double *h_out_dev = nullptr;  // device alias of h_out
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evr = nullptr;   // iteration start/end, rollout end
   bool timed = false;
 };
@@ -335,7 +336,7 @@ int launch_update(bssmppi_ctx *c, bool final_, double *rec_out) {
   if (final_ && c->k_count <= kSmallK && T2 <= kCombinePart) {   // one launch at small K
     update_small_kernel<<<1, kCombThreads, 0, c->stream>>>(c->k_count, c->k_begin, T2, c->d_cost, c->d_u, c->lam,
                                                            c->lo[0], c->lo[1], c->hi[0], c->hi[1], c->d_out,
-                                                           c->d_state + 24, c->d_out + T2);
+                                                           c->d_state + 24, c->d_out + T2, c->h_out_dev);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(BSSMPPI_ERR_CUDA, "update launch: %s", cudaGetErrorString(e));
     return BSSMPPI_OK;
@@ -344,7 +345,7 @@ int launch_update(bssmppi_ctx *c, bool final_, double *rec_out) {
       c->k_count, c->k_begin, T2, c->d_cost, c->d_u, c->lam, c->chunk, c->d_rec);
   combine_kernel<<<1, kCombThreads, 0, c->stream>>>(
       c->nblocks, T2, c->d_rec, c->lam, final_ ? 1 : 0, rec_out, c->lo[0], c->lo[1], c->hi[0],
-      c->hi[1], c->d_out, c->d_state + 24, c->d_out + T2);
+      c->hi[1], c->d_out, c->d_state + 24, c->d_out + T2, final_ ? c->h_out_dev : nullptr);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(BSSMPPI_ERR_CUDA, "update launch: %s", cudaGetErrorString(e));
   return BSSMPPI_OK;
@@ -428,7 +429,7 @@ int run_iteration(bssmppi_ctx *c, RollParams &rp, bool final_, double *rec_out) 
 
 int finish(bssmppi_ctx *c, double *vplus, bssmppi_diag *diag) {
   const int T2 = 2 * c->T;
-  CUDA_TRY(cudaMemcpyAsync(c->h_out, c->d_out, (T2 + kRecHead) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  // the final update kernel wrote v+ and head into mapped h_out as well
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   const double *head = c->h_out + T2;
   if (diag) {
@@ -502,7 +503,8 @@ int bssmppi_create(const bssmppi_problem *problem, int32_t device, bssmppi_ctx *
   if ((rc = dev_alloc(&c->d_rec, (size_t)c->nblocks * (kRecHead + T2)))) return bail(rc);
   if ((rc = dev_alloc(&c->d_out, T2 + kRecHead))) return bail(rc);
   if (cudaMallocHost((void **)&c->h_state, (24 + T2) * sizeof(float)) != cudaSuccess ||
-      cudaMallocHost((void **)&c->h_out, (T2 + kRecHead) * sizeof(double)) != cudaSuccess)
+      cudaHostAlloc((void **)&c->h_out, (T2 + kRecHead) * sizeof(double), cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer((void **)&c->h_out_dev, c->h_out, 0) != cudaSuccess)
     return bail(fail(BSSMPPI_ERR_CUDA, "cudaMallocHost failed"));
   if (cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
       cudaEventCreate(&c->evr) != cudaSuccess)
@@ -614,7 +616,7 @@ int bssmppi_enqueue_combine(bssmppi_ctx *c, const double *partials_dev, int32_t 
   const int T2 = 2 * c->T;
   combine_kernel<<<1, kCombThreads, 0, c->stream>>>(nslots, T2, partials_dev, c->lam, 1, nullptr, c->lo[0],
                                                    c->lo[1], c->hi[0], c->hi[1], c->d_out, c->d_state + 24,
-                                                   c->d_out + T2);
+                                                   c->d_out + T2, c->h_out_dev);
   CUDA_TRY(cudaGetLastError());
   return BSSMPPI_OK;
 }
@@ -680,7 +682,7 @@ int bssmppi_mppi_update(int32_t K, int32_t T, const double *costs, const double 
     if (e == cudaSuccess) {
       update_partials_kernel<double, double><<<nblocks, kUpdThreads>>>(K, 0, T2, d_c, d_u, temperature, chunk, d_rec);
       combine_kernel<<<1, kCombThreads>>>(nblocks, T2, d_rec, temperature, 1, nullptr, lo[0], lo[1], hi[0], hi[1],
-                                         d_out, nullptr, d_out + T2);
+                                         d_out, nullptr, d_out + T2, nullptr);
       e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = cudaMemcpy(h.data(), d_out, h.size() * sizeof(double), cudaMemcpyDeviceToHost);

@@ -113,11 +113,13 @@ update_partials_kernel(int n, int k_begin, int T2, const CT *costs, const UT *u,
 // (deterministic).  final == 0: write one record to rec_out.  final == 1:
 // v+ = clip(N/Z) -> vplus (double), warm-start shifted plan
 // (ControlPlan.shifted, controllers.py:154-156) -> plan_out (float, may be
-// null), head {beta, Z, Z2, n, argmin} -> head_out.
+// null), head {beta, Z, Z2, n, argmin} -> head_out; v+ and head also to
+// `mirror` (host-mapped pinned memory, may be null) so the host reads the
+// result after the stream sync without a separate device-to-host copy.
 __global__ void __launch_bounds__(kCombThreads)
 combine_kernel(int nrec, int T2, const double *rec, double lam, int final_, double *rec_out,
                double lo0, double lo1, double hi0, double hi1, double *vplus, float *plan_out,
-               double *head_out) {
+               double *head_out, double *mirror) {
   __shared__ double s_scale[1024];
   __shared__ double s_part[kCombinePart];
   __shared__ double s_a[kCombThreads], s_b[kCombThreads], s_c[kCombThreads];
@@ -197,11 +199,16 @@ combine_kernel(int nrec, int T2, const double *rec, double lam, int final_, doub
       const double v = a / s_head[1];
       const double l = (col & 1) ? lo1 : lo0, h = (col & 1) ? hi1 : hi0;
       vplus[col] = fmin(fmax(v, l), h);
+      if (mirror != nullptr) mirror[col] = vplus[col];
     }
   }
   if (tid < kRecHead) {
-    if (!final_) rec_out[tid] = s_head[tid];
-    else head_out[tid] = s_head[tid];
+    if (!final_) {
+      rec_out[tid] = s_head[tid];
+    } else {
+      head_out[tid] = s_head[tid];
+      if (mirror != nullptr) mirror[T2 + tid] = s_head[tid];
+    }
   }
   if (final_ && plan_out != nullptr) {
     __syncthreads();
@@ -221,7 +228,8 @@ constexpr int kSmallK = 1024;   // at K = 2048 the two-level update was already 
 
 __global__ void __launch_bounds__(kCombThreads)
 update_small_kernel(int n, int k_begin, int T2, const float *costs, const float *u, double lam, double lo0,
-                    double lo1, double hi0, double hi1, double *vplus, float *plan_out, double *head_out) {
+                    double lo1, double hi0, double hi1, double *vplus, float *plan_out, double *head_out,
+                    double *mirror) {
   __shared__ double s_w[kSmallK];
   __shared__ double s_part[kCombinePart];   // also the reduction scratch of steps 1-2
   __shared__ double s_head[kRecHead];
@@ -296,8 +304,12 @@ update_small_kernel(int n, int k_begin, int T2, const float *costs, const float 
     const double v = a / s_head[1];
     const double l = (col & 1) ? lo1 : lo0, h = (col & 1) ? hi1 : hi0;
     vplus[col] = fmin(fmax(v, l), h);
+    if (mirror != nullptr) mirror[col] = vplus[col];
   }
-  if (tid < kRecHead) head_out[tid] = s_head[tid];
+  if (tid < kRecHead) {
+    head_out[tid] = s_head[tid];
+    if (mirror != nullptr) mirror[T2 + tid] = s_head[tid];
+  }
   if (plan_out != nullptr) {
     __syncthreads();
     for (int col = tid; col < T2; col += kCombThreads) {
