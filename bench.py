@@ -394,7 +394,9 @@ def main():
                 "path": "Controller.control_step (host numpy state/plan -> C ABI -> host v+)"},
         "roofline": roofline,
         "clocks": clock_info,
-        "gpu_launches": 3 * args.steps,
+        # rollout + update partials + combine; a single-context K <= 1024
+        # iteration runs the one-launch update (csrc/update.cuh kSmallK)
+        "gpu_launches": (2 if world == 1 and k_count <= 1024 else 3) * args.steps,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, cores, sample = cpu_rate(wl, args.cpu_seconds)
