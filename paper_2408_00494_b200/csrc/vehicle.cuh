@@ -222,7 +222,7 @@ struct StepShared {
 // the belief mean's frame check).
 __device__ __forceinline__ StepShared step_shared(const float x[8], const CtlDev &c, const VehDev &V,
                                                   const TrackDev &tr, float kap) {
-  const float vx = x[0], wf = x[3], wr = x[4], s = x[7];
+  const float vx = x[0], wf = x[3], wr = x[4];
   StepShared h;
   // _tire_row: low-speed floor keeps the sign of vx.
   h.vxe = (vx >= 0.f) ? fmaxf(vx, V.vfloor) : fminf(vx, -V.vfloor);
