@@ -265,6 +265,15 @@ void fill_params(bssmppi_ctx *c, const bssmppi_problem *p) {
 // or a tied G on every one.  Decided on the LOCAL rollout count, so a
 // K-shard of 2048 rollouts (C3 over 8 GPUs) keeps one warp per rollout;
 // across world sizes the moment sums may then differ by FP32 summation order.
+#ifndef BSS_BIG_MIN_WARPS
+#define BSS_BIG_MIN_WARPS 1900
+#endif
+#ifndef BSS_BIG_MAX_WARPS
+#define BSS_BIG_MAX_WARPS 2368
+#endif
+constexpr long long kBigBlockMinWarps = BSS_BIG_MIN_WARPS;   // 512-thread blocks for
+constexpr long long kBigBlockMaxWarps = BSS_BIG_MAX_WARPS;   // [min, max] warps per launch
+
 int group_width(int M, int K) {
   static const int forced = [] {   // tuning override (tools/g_sweep.py); 0 = policy
     const char *e = std::getenv("BSSMPPI_FORCE_G");
@@ -292,20 +301,42 @@ int rollout_group_width(int M, int K, bool persist) {
   return g;
 }
 
+// Block size of the belief kernel: 128 threads (4 blocks per SM) in
+// general; 512 (one block per SM, same registers and occupancy) when the
+// launch is one nearly full wave (1900-2368 warps): the 8-GPU shards of C3
+// and C4 and the C2 control step ran 4-5% faster that way, while 1024-warp
+// launches (half the SMs left idle with 512-thread blocks) and multi-wave
+// ones ran slower (tools/block_sweep.sh, profiles/r1_block_sweep.txt).
+// BSSMPPI_FORCE_BLOCK overrides (sweeps).
+int rollout_block_threads(int k_count, int G, bool persist, bool zarr) {
+  static const int forced = [] {
+    const char *e = std::getenv("BSSMPPI_FORCE_BLOCK");
+    return e ? std::atoi(e) : 0;
+  }();
+  // persist: clouds sized per 128-thread block; zarr (parity runs): 128 only
+  if (persist || zarr) return kBlockThreads;
+  if (forced == kBlockThreads || forced == kMaxBlockThreads) return forced;
+  const long long warps = (long long)k_count * G / 32;
+  return (warps >= kBigBlockMinWarps && warps <= kBigBlockMaxWarps) ? kMaxBlockThreads : kBlockThreads;
+}
+
 template <int G>
 cudaError_t launch_bss_g(const RollParams &rp, bool persist, bool zarr, cudaStream_t st) {
-  constexpr int GPB = kBlockThreads / G;   // rollouts per block
+  const int threads = rollout_block_threads(rp.k_count, G, persist, zarr);
+  const int GPB = threads / G;   // rollouts per block
   const int blocks = (rp.k_count + GPB - 1) / GPB;
-  size_t smem = (size_t)(kBlockThreads / 32) * (32 / G) * 2 * kSlotFloats * sizeof(float);
+  size_t smem = (size_t)(threads / 32) * (32 / G) * 2 * kSlotFloats * sizeof(float);
   if (persist) smem += (size_t)GPB * 8 * rp.M * sizeof(float);
   void (*fn)(const RollParams);
   if (persist) fn = zarr ? bss_rollout_kernel<G, true, true> : bss_rollout_kernel<G, true, false>;
-  else fn = zarr ? bss_rollout_kernel<G, false, true> : bss_rollout_kernel<G, false, false>;
+  else if (zarr) fn = bss_rollout_kernel<G, false, true>;
+  else if (threads == kMaxBlockThreads) fn = bss_rollout_kernel<G, false, false, kMaxBlockThreads>;
+  else fn = bss_rollout_kernel<G, false, false>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  fn<<<blocks, kBlockThreads, smem, st>>>(rp);
+  fn<<<blocks, threads, smem, st>>>(rp);
   return cudaGetLastError();
 }
 

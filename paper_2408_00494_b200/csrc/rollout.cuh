@@ -298,6 +298,10 @@ constexpr int kSlotFloats = 20;   // 18 sums, 16-byte aligned slot
 #define BSS_BLOCK_THREADS 128
 #endif
 constexpr int kBlockThreads = BSS_BLOCK_THREADS;
+// The belief kernel is also instantiated for 512-thread blocks (same
+// 128-register budget: one block fills an SM's register file); see
+// bssmppi.cu rollout_block_threads for when it is launched.
+constexpr int kMaxBlockThreads = 512;
 // Register budget: 4 resident 128-thread blocks per SM (<= 128 registers,
 // 16 warps/SM).  With the software-pipelined noise (particle_pass) the extra
 // registers buy more than occupancy: 5 / 6 / 7 blocks per SM (96 / 80 / 72
@@ -486,21 +490,22 @@ __device__ __forceinline__ void particle_pass(const RollParams &P, int t, int k,
 // ZARR: read the reference's normals instead of Philox; NK: the process
 // noise kind (NoiseKind), resolved once at kernel entry so every variant's
 // T loop holds exactly one particle loop (register allocation per variant).
-template <int G, bool PERSIST, bool ZARR, int NK, bool ST>
+template <int G, bool PERSIST, bool ZARR, int NK, bool ST, int BT>
 __device__ __forceinline__ void bss_rollout(const RollParams &P) {
   extern __shared__ float4 smem4[];
   float *smem = reinterpret_cast<float *>(smem4);
   constexpr int GPW = 32 / G;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gi = lane / G, li = lane % G;
-  const int warp_global = blockIdx.x * (kBlockThreads / 32) + warp;
+  constexpr int nwarps = BT / 32;
+  const int warp_global = blockIdx.x * nwarps + warp;
   if (warp_global * GPW >= P.k_count) return;            // whole warp idle
   const int kraw = warp_global * GPW + gi;
   const bool active = kraw < P.k_count;
   const int k = active ? kraw : P.k_count - 1;            // keep shuffles convergent
   const int kg = P.k_begin + k;
   float *slots = smem + (warp * GPW + gi) * 2 * kSlotFloats;
-  float *cloud = PERSIST ? smem + (kBlockThreads / 32) * GPW * 2 * kSlotFloats +
+  float *cloud = PERSIST ? smem + nwarps * GPW * 2 * kSlotFloats +
                                (size_t)(warp * GPW + gi) * 8 * P.M
                          : nullptr;
 
@@ -606,21 +611,23 @@ __device__ __forceinline__ void bss_rollout(const RollParams &P) {
 #ifdef BSS_MAXNREG
 #define BSS_ROLLOUT_BOUNDS __maxnreg__(BSS_MAXNREG)
 #else
-#define BSS_ROLLOUT_BOUNDS __launch_bounds__(kBlockThreads, BSS_MIN_BLOCKS)
+#define BSS_ROLLOUT_BOUNDS __launch_bounds__(BT, kBlockThreads * BSS_MIN_BLOCKS / BT)
 #endif
 // Kernel-entry dispatch on the launch-constant noise kind and tire-sine
 // range: every variant's T loop holds exactly one particle loop.
-template <int G, bool PERSIST, bool ZARR, bool ST>
+template <int G, bool PERSIST, bool ZARR, bool ST, int BT>
 __device__ __forceinline__ void bss_rollout_nk(const RollParams &P) {
-  if (!ZARR && P.noise_kind == 1) bss_rollout<G, PERSIST, ZARR, NK_LAPLACE, ST>(P);
-  else if (P.noise_diag) bss_rollout<G, PERSIST, ZARR, NK_GAUSS_DIAG, ST>(P);
-  else bss_rollout<G, PERSIST, ZARR, NK_GAUSS_GENERAL, ST>(P);
+  if (!ZARR && P.noise_kind == 1) bss_rollout<G, PERSIST, ZARR, NK_LAPLACE, ST, BT>(P);
+  else if (P.noise_diag) bss_rollout<G, PERSIST, ZARR, NK_GAUSS_DIAG, ST, BT>(P);
+  else bss_rollout<G, PERSIST, ZARR, NK_GAUSS_GENERAL, ST, BT>(P);
 }
 
-template <int G, bool PERSIST, bool ZARR>
+// BT: block threads, a compile-time constant (128, or 512 for the one-wave
+// shapes of bssmppi.cu rollout_block_threads); same register budget.
+template <int G, bool PERSIST, bool ZARR, int BT = kBlockThreads>
 __global__ void BSS_ROLLOUT_BOUNDS bss_rollout_kernel(const RollParams P) {
-  if (P.V.tire_short) bss_rollout_nk<G, PERSIST, ZARR, true>(P);
-  else bss_rollout_nk<G, PERSIST, ZARR, false>(P);
+  if (P.V.tire_short) bss_rollout_nk<G, PERSIST, ZARR, true, BT>(P);
+  else bss_rollout_nk<G, PERSIST, ZARR, false, BT>(P);
 }
 
 // Deterministic rollouts for kind "mppi" / "smppi" (controllers.py:320-338):
