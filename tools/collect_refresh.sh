@@ -4,9 +4,10 @@
 # summary and the per-line instruction breakdown of the C3 rollout kernel.
 set -e
 cd "$(dirname "$0")/.."
-K=_ZN3bss18bss_rollout_kernelILi8ELb0ELb0EEEvNS_10RollParamsE
 tmp=$(mktemp -d)
 (cd "$tmp" && cuobjdump -xelf all "$OLDPWD/paper_2408_00494_b200/libbssmppi.so" > /dev/null && nvdisasm -g bssmppi.sm_100a.cubin > all.sass)
+# the C3 launch: G = 8, Philox noise, 128-thread blocks
+K=$(grep -o '^\.text\._ZN3bss18bss_rollout_kernelILi8ELb0ELb0ELi128EEEvNS_10RollParamsE' "$tmp/all.sass" | head -1 | sed 's/^\.text\.//')
 python tools/ncu_summary.py gpurun_out/r_prof_c3.ncu-rep 209715200 \
   "r1 ncu summary — bss_rollout_kernel<8,false,false> (G=8: 4 rollouts per warp, 32 particles per lane), C3 (K=16384, M=256, T=50)" \
   "ncu --set full --clock-control none --import-source on -k regex:bss_rollout -s 1 -c 1 python tools/profile_iter.py --iters 2" \
