@@ -3,7 +3,9 @@ noise arrays would be multi-GB: the device (Philox mode) against the FP64 C
 oracle driving the SAME Philox4x32 counters on the host (oracle/bss_oracle.c,
 pinned to the reference by tests/test_c_oracle.py).  The two differ only by
 FP32 vs FP64 arithmetic and MUFU vs libm Box-Muller (~1e-7 on the normals).
-These shapes exercise the narrowed lane groups (G = 8) of large K."""
+These shapes exercise the narrowed lane groups (G = 8) of large K and the
+512-thread one-wave launches (C2; a ragged 2047-rollout shard whose last
+block is partial)."""
 
 import numpy as np
 import pytest
@@ -16,8 +18,9 @@ from paper_2408_00494_b200.tracks import named_track
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("K,M,T,dt", [(16384, 256, 50, 0.04), (32768, 64, 60, 0.04), (4096, 128, 40, 0.05)],
-                         ids=["C3", "C5_32768x64", "C2"])
+@pytest.mark.parametrize("K,M,T,dt", [(16384, 256, 50, 0.04), (32768, 64, 60, 0.04), (4096, 128, 40, 0.05),
+                                     (2047, 256, 20, 0.05)],
+                         ids=["C3", "C5_32768x64", "C2", "ragged_one_wave"])
 def test_fullsize_philox_costs_and_update(K, M, T, dt):
     track = named_track("spline0" if dt == 0.04 else "ellipse")
     model = md.with_timestep(md.VehicleParams(), dt, "euler")
