@@ -355,6 +355,8 @@ def main():
         tj = json.loads(tpath.read_text())
         traffic = tj.get(args.workload)
     G = _lib.load().bssmppi_group_width(wl["M"], k_count)
+    warps = k_count * G // 32   # csrc/bssmppi.cu rollout_block_threads: one-wave launches use 512
+    block = 512 if 1900 <= warps <= 2368 else 128
     fp32 = {"achieved": achieved, "peak": peak, "unit": "TFLOP/s",
             "frac": achieved / peak if peak else None,
             "peak_source": "FFMA microbenchmark measured in this run (MEASURED_PEAKS.json has "
@@ -375,7 +377,7 @@ def main():
     # HBM (HBM is < 1 % here: 70 KB of DRAM traffic per launch)
     bind = sfu if (sfu["frac"] or 0) > (fp32["frac"] or 0) else fp32
     roofline = {"bound": "sfu" if bind is sfu else "fp32",
-                "kernel": f"bss_rollout_kernel<{G},false,false>",
+                "kernel": f"bss_rollout_kernel<{G},false,false,{block}>",
                 "achieved": bind["achieved"], "peak": bind["peak"], "unit": bind["unit"],
                 "frac": bind["frac"], "traffic": traffic,
                 "rollout_ms": roll_avg, "rollout_share_of_step": roll_avg / statistics.mean(step_ms),
