@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define BSSMPPI_ABI_VERSION 2
+#define BSSMPPI_ABI_VERSION 3
 
 typedef enum {
   BSSMPPI_OK = 0,
@@ -102,6 +102,10 @@ typedef struct bssmppi_problem {
   const double *centerline;      /* rows x 3: x, y, theta at s = i * centerline_ds */
   int32_t centerline_n;
   double centerline_ds;
+  /* ---- Launch shape (not a reference parameter): lanes per rollout of the
+   * bss kernel, 0 = the measured policy (bssmppi_group_width), else 2, 4, 8,
+   * 16 or 32 -- lets the parity tests pin the production widths. */
+  int32_t group_width;
 } bssmppi_problem;
 
 /* Diagnostics of one iteration (the reference returns none; north_star asks). */
@@ -115,14 +119,18 @@ typedef struct bssmppi_diag {
   float rollout_ms;         /* ... of which the fused rollout kernel */
 } bssmppi_diag;
 
-typedef struct bssmppi_ctx bssmppi_ctx;
-
 const char *bssmppi_last_error(void);
 int32_t bssmppi_abi_version(void);
 /* Size of one K-shard partial record: 5 + 2*horizon doubles. */
 int32_t bssmppi_partial_len(int32_t horizon);
 /* Lanes per rollout the bss kernel uses for (M, local rollout count). */
 int32_t bssmppi_group_width(int32_t inner_samples, int32_t k_count);
+
+typedef struct bssmppi_ctx bssmppi_ctx;
+/* The bss kernel's launch shape for this context: lanes per rollout (1 for
+ * the deterministic kinds) and threads per block, as the next launch will
+ * use them (policy, problem.group_width, BSSMPPI_FORCE_BLOCK). */
+int32_t bssmppi_launch_shape(const bssmppi_ctx *ctx, int32_t *group_width, int32_t *block_threads);
 
 int bssmppi_create(const bssmppi_problem *problem, int32_t device, bssmppi_ctx **out);
 void bssmppi_destroy(bssmppi_ctx *ctx);

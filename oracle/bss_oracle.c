@@ -178,15 +178,25 @@ static void bm(uint32_t a, uint32_t b, double *z0, double *z1) {
   *z1 = r * sin(2.0 * M_PI * u2);
 }
 
+/* Belief stream (csrc/philox.cuh belief_block / box_muller_word): ONE
+ * Philox4x32-7 block per particle-step, counter (t, m, kg, 0); word i ->
+ * pair i with u1 = 1 - (n + 1/2) 2^-20 (n = top 20 bits) and angle
+ * 2 pi j / 4096 (j = low 12 bits); standard pair -sqrt(-2 ln u1)(cos, sin). */
+static void bm_word(uint32_t w, double *z0, double *z1) {
+  double u1 = 1.0 - ((double)(w >> 12) + 0.5) * (1.0 / 1048576.0);
+  double th = 2.0 * M_PI * (double)(w & 0xfffu) / 4096.0;
+  double r = sqrt(-2.0 * log(u1));
+  *z0 = -r * cos(th);
+  if (z1) *z1 = -r * sin(th);
+}
+
 static void belief_normals(uint32_t k0, uint32_t k1, uint32_t t, uint32_t kg, uint32_t m, double z[7]) {
-  uint32_t a[4] = {t, m, kg, 0u}, b[4] = {t, m, kg, 1u};
-  double spare;
+  uint32_t a[4] = {t, m, kg, 0u};
   philox_r(a, k0, k1, 7);
-  philox_r(b, k0, k1, 7);
-  bm(a[0], a[1], &z[0], &z[1]);
-  bm(a[2], a[3], &z[2], &z[3]);
-  bm(b[0], b[1], &z[4], &z[5]);
-  bm(b[2], b[3], &z[6], &spare);
+  bm_word(a[0], &z[0], &z[1]);
+  bm_word(a[1], &z[2], &z[3]);
+  bm_word(a[2], &z[4], &z[5]);
+  bm_word(a[3], &z[6], NULL);
 }
 
 static void control_normals(uint32_t k0, uint32_t k1, uint32_t t, uint32_t kg, double *z0, double *z1) {
@@ -220,20 +230,23 @@ int orc_philox4x32(const uint32_t ctr[4], const uint32_t key[2], int rounds, uin
 
 /* Config-4 extension (beyond the reference; obstacles.py): Laplace + slip
  * noise from the second Philox block's words, obstacle heuristic terms. */
-static double centred_uniform(uint32_t w) { return ((double)(w >> 9) + 0.5) * (1.0 / 8388608.0) - 0.5; }
+/* centred uniform (n + 1/2) 2^-16 - 1/2 of a 16-bit field n */
+static double centred_uniform16(uint32_t n) { return ((double)n + 0.5) * (1.0 / 65536.0) - 0.5; }
 
+/* csrc/philox.cuh laplace_from_block: normals from words 0, 1; Laplace on
+ * (vx, vy, r) and the vy slip from the 16-bit halves of words 2, 3. */
 static void belief_noise_laplace(uint32_t k0, uint32_t k1, uint32_t t, uint32_t kg, uint32_t m, double b,
                                  double a, double z[4], double w[3]) {
-  uint32_t p[4] = {t, m, kg, 0u}, q[4] = {t, m, kg, 1u};
+  uint32_t p[4] = {t, m, kg, 0u};
   philox_r(p, k0, k1, 7);
-  philox_r(q, k0, k1, 7);
-  bm(p[0], p[1], &z[0], &z[1]);
-  bm(p[2], p[3], &z[2], &z[3]);
+  bm_word(p[0], &z[0], &z[1]);
+  bm_word(p[1], &z[2], &z[3]);
+  const uint32_t f[4] = {p[2] >> 16, p[2] & 0xffffu, p[3] >> 16, p[3] & 0xffffu};
   for (int i = 0; i < 3; ++i) {
-    double u = centred_uniform(q[i]);
+    double u = centred_uniform16(f[i]);
     w[i] = -b * copysign(log(1.0 - 2.0 * fabs(u)), u);
   }
-  w[1] += 2.0 * a * centred_uniform(q[3]);
+  w[1] += 2.0 * a * centred_uniform16(f[3]);
 }
 
 static double obstacle_terms(const bssmppi_problem *p, double s, double ey, double sigy, int *inside) {
@@ -282,6 +295,7 @@ typedef struct {
   const double *x0, *cov0, *nominal, *u_in, *eps_in, *z_in;
   uint32_t kc[2], kb[2];
   int philox_ctrl, philox_belief;
+  double *mom_out;   /* (T, k_count, 18): mean[8] + upper cov (00,01,02,03,11,12,13,22,23,33), or NULL */
 } Inputs;
 
 /* One rollout k (local index); returns its cost, writes u_out row. */
@@ -361,6 +375,13 @@ static double rollout_one(const Ctx *c, const Inputs *in, int k, double *xs, dou
     }
     double mu[8], cv[16];
     moments(xs, M, buf, mu, cv);
+    if (in->mom_out) {
+      double *mo = in->mom_out + ((size_t)t * K + k) * 18;
+      for (int i = 0; i < 8; ++i) mo[i] = mu[i];
+      int q = 8;
+      for (int a = 0; a < 4; ++a)
+        for (int b = a; b < 4; ++b) mo[q++] = cv[a * 4 + b];
+    }
     int ok = 1;
     for (int i = 0; i < 8; ++i) ok &= isfinite(mu[i]);
     for (int i = 0; i < 16; ++i) ok &= isfinite(cv[i]);
@@ -384,10 +405,12 @@ static double rollout_one(const Ctx *c, const Inputs *in, int k, double *xs, dou
   return dead ? INFINITY : total;
 }
 
-/* Rollout costs for the context's k-range.  Noise arrays override Philox. */
-int orc_rollout(const bssmppi_problem *p, const double *x0, const double *cov0, const double *nominal,
-                const double *u_in, const double *eps_in, const double *z_in, const uint32_t key_ctrl[2],
-                const uint32_t key_belief[2], double *costs, double *u_out, int nthreads) {
+/* Rollout costs for the context's k-range.  Noise arrays override Philox.
+ * mom_out (nullable): the per-step belief moments, (T, k_count, 18). */
+int orc_rollout_moments(const bssmppi_problem *p, const double *x0, const double *cov0, const double *nominal,
+                        const double *u_in, const double *eps_in, const double *z_in, const uint32_t key_ctrl[2],
+                        const uint32_t key_belief[2], double *costs, double *u_out, double *mom_out,
+                        int nthreads) {
   double ph[23];
   memcpy(ph, p->phys, sizeof(ph));
   Ctx c = {p, ph};
@@ -396,6 +419,7 @@ int orc_rollout(const bssmppi_problem *p, const double *x0, const double *cov0, 
   in.x0 = x0; in.cov0 = cov0; in.nominal = nominal; in.u_in = u_in; in.eps_in = eps_in; in.z_in = z_in;
   in.philox_ctrl = eps_in == NULL;
   in.philox_belief = z_in == NULL;
+  in.mom_out = mom_out;
   if (key_ctrl) { in.kc[0] = key_ctrl[0]; in.kc[1] = key_ctrl[1]; }
   if (key_belief) { in.kb[0] = key_belief[0]; in.kb[1] = key_belief[1]; }
   const int M = p->kind == BSSMPPI_KIND_BSS ? p->inner_samples : 1;
@@ -412,6 +436,13 @@ int orc_rollout(const bssmppi_problem *p, const double *x0, const double *cov0, 
     free(buf);
   }
   return 0;
+}
+
+int orc_rollout(const bssmppi_problem *p, const double *x0, const double *cov0, const double *nominal,
+                const double *u_in, const double *eps_in, const double *z_in, const uint32_t key_ctrl[2],
+                const uint32_t key_belief[2], double *costs, double *u_out, int nthreads) {
+  return orc_rollout_moments(p, x0, cov0, nominal, u_in, eps_in, z_in, key_ctrl, key_belief, costs, u_out, NULL,
+                             nthreads);
 }
 
 /* mppi_weights + mppi_update (controllers.py:180-194).  Returns 3 if no

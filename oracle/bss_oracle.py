@@ -84,7 +84,7 @@ def derivs(x, u0, u1, p, track):
     cos_d, sin_d = np.cos(u0), np.sin(u0)
     fxf_b = fxf * cos_d - fyf * sin_d
     fyf_b = fxf * sin_d + fyf * cos_d
-    dx = np.empty(x.shape)
+    dx = np.empty(x.shape, x.dtype)
     dx[..., 0] = (fxf_b + fxr) / p[0] + vy * r
     dx[..., 1] = (fyf_b + fyr) / p[0] - vx * r
     dx[..., 2] = (p[2] * fyf_b - p[3] * fyr) / p[1]
@@ -231,6 +231,23 @@ class Problem:
         return cls(ctx.model, ctx.track, c.q_diag, c.v_goal, c.obstacle_penalty,
                    c.terminal_scale, c.safety.cbf_rate, c.safety.penalty, c.backoff, F)
 
+    def astype(self, dtype):
+        """Copy whose constants and track tables are ``dtype`` (FP32
+        emulation of the reference, tests/test_fp32_conditioning.py): numpy
+        then evaluates the reference's formulas in that precision."""
+        import copy
+        import types
+        out = copy.copy(self)
+        out.p = self.p.astype(dtype)
+        out.dt = dtype(self.dt)
+        out.q = self.q.astype(dtype)
+        out.F = self.F.astype(dtype)
+        tr = self.track
+        out.track = types.SimpleNamespace(s=np.asarray(tr.s, dtype), kappa=np.asarray(tr.kappa, dtype),
+                                          length=dtype(tr.length), closed=tr.closed,
+                                          half_width=dtype(tr.half_width))
+        return out
+
     def stage(self, x):
         return stage_cost(x, self.q, self.v_goal, self.c_obs, self.track.half_width)
 
@@ -239,16 +256,27 @@ class Problem:
 
 
 def rollout_bss(prob: Problem, x0, cov0, u, eps, nominal, z_all, precision=None,
-                gamma=0.0, persist=False, record=None):
+                gamma=0.0, persist=False, record=None, dtype=np.float64, round_state=None):
     """Belief rollout costs (``_rollout`` bss branch, controllers.py:261-319, 340).
 
     u: (K, T, 2) clamped controls, eps: (K, T, 2) raw perturbations,
     z_all: (T, K, M, 7) standard normals.  ``record`` (list) receives
-    (mean, cov, ok) per step like the reference's propagate_mc_batch."""
+    (mean, cov, ok) per step like the reference's propagate_mc_batch.
+    ``dtype=np.float32`` evaluates the same algorithm (dynamics, tree mean,
+    two-pass covariance, Cholesky) in FP32 -- the SURVEY A4 emulation that
+    separates FP32's own conditioning from device deviations.
+    ``round_state=np.float32`` keeps FP64 arithmetic but rounds every
+    particle state to FP32 after the re-projection and after the step: the
+    irreducible error of holding particles in FP32 registers."""
+    rnd = (lambda a: a) if round_state is None else (lambda a: a.astype(round_state).astype(a.dtype))
     K, T, _ = u.shape
     M = z_all.shape[2]
-    x0 = np.asarray(x0, float)
-    cov0 = np.asarray(cov0, float)
+    if dtype is not np.float64:
+        prob = prob.astype(dtype)
+        u = np.asarray(u, dtype)
+        z_all = np.asarray(z_all, dtype)
+    x0 = np.asarray(x0, dtype)
+    cov0 = np.asarray(cov0, dtype)
     precision = np.zeros((2, 2)) if precision is None else precision
     total = control_cost(np.asarray(nominal, float), eps, precision, gamma)
     dead = np.zeros(K, dtype=bool)
@@ -272,10 +300,12 @@ def rollout_bss(prob: Problem, x0, cov0, u, eps, nominal, z_all, precision=None,
             L = chol_psd(covs)
             x = np.repeat(means[:, None, :], M, axis=1)
             x[:, :, SUBSET] += np.einsum("kab,kmb->kma", L, z_all[t][:, :, :4])
+        x = rnd(x)
         ub = np.repeat(u[:, t][:, None, :], M, axis=1)
         x1, _ = step_euler(x, ub, prob.p, prob.track, prob.dt)   # per-particle ok discarded
         if noise_on:                                      # dynamics.py:571-572
             x1[..., 0:3] += z_all[t][:, :, 4:7] @ prob.F.T
+        x1 = rnd(x1)
         if persist:
             cloud = x1
         mean1, cov1 = moments(x1)

@@ -29,6 +29,8 @@ def load():
         from paper_2408_00494_b200._lib import Problem
         lib.orc_rollout.argtypes = [C.POINTER(Problem), _dp, _dp, _dp, _dp, _dp, _dp, _u32p, _u32p,
                                     _dp, _dp, C.c_int]
+        lib.orc_rollout_moments.argtypes = [C.POINTER(Problem), _dp, _dp, _dp, _dp, _dp, _dp, _u32p,
+                                            _u32p, _dp, _dp, _dp, C.c_int]
         lib.orc_update.argtypes = [C.c_int, C.c_int, _dp, _dp, C.c_double, _dp, _dp, _dp]
         lib.orc_control_step.argtypes = [C.POINTER(Problem), _dp, _dp, _dp, _u32p, _u32p, _dp, _dp,
                                          _dp, C.c_int]
@@ -49,17 +51,21 @@ def _key(k):
 
 
 def rollout(problem, x0, cov0, nominal, u=None, eps=None, z=None, key_ctrl=None, key_belief=None,
-            threads=0):
-    """Costs (k_count,) and the clamped controls used (k_count, T, 2)."""
+            threads=0, moments=False):
+    """Costs (k_count,) and the clamped controls used (k_count, T, 2); with
+    ``moments=True`` also the per-step belief moments (T, k_count, 18):
+    mean[8] then the covariance upper triangle (the device layout)."""
     lib = load()
     K, T = problem.k_count, problem.horizon
     keep = [np.ascontiguousarray(a, dtype=np.float64) if a is not None else None
             for a in (x0, cov0, nominal, u, eps, z)]
     costs = np.empty(K)
     u_out = np.empty((K, T, 2))
-    lib.orc_rollout(C.byref(problem), *[_p(a) for a in keep], _key(key_ctrl), _key(key_belief),
-                    costs.ctypes.data_as(_dp), u_out.ctypes.data_as(_dp), int(threads))
-    return costs, u_out
+    mom = np.empty((T, K, 18)) if moments else None
+    lib.orc_rollout_moments(C.byref(problem), *[_p(a) for a in keep], _key(key_ctrl), _key(key_belief),
+                            costs.ctypes.data_as(_dp), u_out.ctypes.data_as(_dp),
+                            None if mom is None else mom.ctypes.data_as(_dp), int(threads))
+    return (costs, u_out, mom) if moments else (costs, u_out)
 
 
 def update(costs, u, lam, lo, hi):

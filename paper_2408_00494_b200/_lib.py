@@ -51,6 +51,7 @@ class Problem(C.Structure):
         ("n_obstacles", C.c_int32), ("obstacles", C.POINTER(C.c_double)),
         ("obstacle_backoff", C.c_double), ("centerline", C.POINTER(C.c_double)),
         ("centerline_n", C.c_int32), ("centerline_ds", C.c_double),
+        ("group_width", C.c_int32),
     ]
 
 
@@ -75,6 +76,7 @@ SIGNATURES = {
     "bssmppi_abi_version": (C.c_int32, []),
     "bssmppi_partial_len": (C.c_int32, [C.c_int32]),
     "bssmppi_group_width": (C.c_int32, [C.c_int32, C.c_int32]),
+    "bssmppi_launch_shape": (C.c_int32, [_ctx, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "bssmppi_create": (C.c_int, [C.POINTER(Problem), C.c_int32, C.POINTER(_ctx)]),
     "bssmppi_destroy": (None, [_ctx]),
     "bssmppi_set_stream": (C.c_int, [_ctx, C.c_void_p]),
@@ -112,7 +114,10 @@ def load():
         if not LIB_PATH.exists():
             raise BssMppiError(ERR_CUDA, f"{LIB_PATH} not built; run __graft_entry__.build()")
         lib = C.CDLL(os.fspath(LIB_PATH))
+        variant = "BSSMPPI_LIB" in os.environ   # A/B builds of older revisions (tools/)
         for name, (res, args) in SIGNATURES.items():
+            if variant and not hasattr(lib, name):
+                continue
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args

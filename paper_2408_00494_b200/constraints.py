@@ -4,8 +4,9 @@ Host side only computes the back-off nu once (reference
 ``constraints.py:70-93``); the per-step DCBF ``track_dcbf_values``
 (``constraints.py:130-137``) and the shield penalty ``penalty_values``
 (``constraints.py:172-186``) are evaluated on the belief moments inside the
-rollout kernel (``csrc/bss_rollout.cuh``).  The numpy forms below are kept
-for API compatibility with callers of the reference module.
+rollout kernel (``csrc/rollout.cuh`` dcbf / shield_penalty); the host-side
+safety bookkeeping of the closed loop (``sim.SafetyMonitor``) restates them
+in FP64 where it needs them.
 """
 
 import math
@@ -53,23 +54,3 @@ def backoff_gaussian(p: float) -> float:
     if not 0.0 < p <= 0.5:
         raise InvalidProbability(f"probability {p} outside (0, 0.5]")
     return float(math.sqrt(2.0) * erfinv(1.0 - 2.0 * p))
-
-
-def backoff_cantelli(p: float) -> float:
-    if not 0.0 < p < 1.0:
-        raise InvalidProbability(f"probability {p} outside (0, 1)")
-    return math.sqrt((1.0 - p) / p)
-
-
-def track_dcbf_values(e_y, sigma_y, half_width: float, nu: float):
-    margin = np.clip(half_width - nu * np.asarray(sigma_y, dtype=float), 0.0, None)
-    return margin * margin - np.square(np.asarray(e_y, dtype=float))
-
-
-def residual_values(h_current, h_previous, cbf_rate: float):
-    return np.asarray(h_current) - (1.0 - cbf_rate) * np.asarray(h_previous)
-
-
-def penalty_values(h_current, h_previous, params):
-    r = residual_values(h_current, h_previous, params.cbf_rate)
-    return params.penalty * np.clip(-r, 0.0, None)

@@ -189,9 +189,10 @@ def _check_supported(ctx, cost):
 
 
 def build_problem(kind, K, T, M, temperature, gamma, sigma_eps, precision, bounds, persist,
-                  ctx, k_begin=0, k_count=None):
+                  ctx, k_begin=0, k_count=None, group_width=0):
     """Pack reference-typed objects into the C ``bssmppi_problem``.
-    Returns (problem, keepalive) -- the track arrays must outlive create()."""
+    Returns (problem, keepalive) -- the track arrays must outlive create().
+    ``group_width`` pins the bss kernel's lanes per rollout (0 = policy)."""
     cost = ctx.cost
     _check_supported(ctx, cost)
     p = _lib.Problem()
@@ -229,6 +230,7 @@ def build_problem(kind, K, T, M, temperature, gamma, sigma_eps, precision, bound
     p.track_closed = int(bool(ctx.track.closed))
     p.k_begin = int(k_begin)
     p.k_count = int(K - k_begin if k_count is None else k_count)
+    p.group_width = int(group_width)
     keep = [s, kap]
     # config-4 extensions (obstacles.py) -- beyond the reference
     if getattr(ctx.noise, "kind", "gaussian") == "laplace_slip":
@@ -335,7 +337,7 @@ class DeviceKey(tuple):
 
 
 def _rollout(kind, x0, cov0, batch, nominal, ctx, precision, cost_weight, rng=None,
-             inner_samples=0, persist_particles=False, moments=False, device=0):
+             inner_samples=0, persist_particles=False, moments=False, device=0, group_width=0):
     u = np.ascontiguousarray(batch.controls, dtype=np.float64)
     eps = np.ascontiguousarray(batch.perturbations, dtype=np.float64)
     K, T, _ = u.shape
@@ -343,7 +345,7 @@ def _rollout(kind, x0, cov0, batch, nominal, ctx, precision, cost_weight, rng=No
         raise ValueError("bss rollouts need an rng and inner_samples >= 2")
     M = int(inner_samples) if kind == "bss" else 1
     prob, keep = build_problem(kind, K, T, M, 1.0, cost_weight, np.eye(2), precision,
-                               ControlBounds(), persist_particles, ctx)
+                               ControlBounds(), persist_particles, ctx, group_width=group_width)
     dc = DeviceContext(prob, device)
     z = key = None
     if kind == "bss":
@@ -375,13 +377,16 @@ def rollout_smppi(x0, batch, nominal, ctx, precision=None, cost_weight: float = 
 
 
 def rollout_bss(mean0, cov0, batch, nominal, ctx, rng, inner_samples: int, precision=None,
-                cost_weight: float = 0.0, persist_particles: bool = False, moments: bool = False):
+                cost_weight: float = 0.0, persist_particles: bool = False, moments: bool = False,
+                group_width: int = 0):
     """Belief-space rollout costs (reference controllers.py:252-258).  With a
     numpy ``rng`` the reference's own normals are consumed; with a
     ``DeviceKey`` the in-kernel Philox generator is used.  ``moments=True``
-    additionally returns the per-step raw belief moments (T, K, 18)."""
+    additionally returns the per-step raw belief moments (T, K, 18).
+    ``group_width`` (not a reference parameter) pins the kernel's lanes per
+    rollout (2..32; 0 = the launch policy)."""
     return _rollout("bss", mean0, cov0, batch, nominal, ctx, precision, cost_weight, rng,
-                    inner_samples, persist_particles, moments)
+                    inner_samples, persist_particles, moments, group_width=group_width)
 
 
 # ---------------------------------------------------------------- controller
@@ -391,7 +396,8 @@ class Controller:
 
     Extra keyword-only options (defaults keep the reference call shape):
     ``noise_source`` ("philox" | "reference"), ``device`` (CUDA ordinal),
-    ``stream`` (cudaStream_t as int), ``obstacles`` (config-4 extension,
+    ``stream`` (cudaStream_t as int), ``group_width`` (lanes per rollout of
+    the bss kernel, 0 = the launch policy), ``obstacles`` (config-4 extension,
     ``obstacles.Obstacles``; with ``noise=obstacles.LaplaceSlipNoise(...)``
     this is BASELINE config 4, beyond the reference).  After each ``control_step`` the
     attribute ``last_diagnostics`` holds v+, the cost minimum/argmin, the
@@ -401,7 +407,7 @@ class Controller:
 
     def __init__(self, config, cost, model, track, noise=None, subset=None, seed: int = 0,
                  run_path=(), *, noise_source: str = "philox", device: int = 0, stream=None,
-                 obstacles=None):
+                 obstacles=None, group_width: int = 0):
         if noise_source not in NOISE_SOURCES:
             raise ValueError(f"noise_source must be one of {NOISE_SOURCES}")
         if noise_source == "reference" and getattr(noise, "kind", "gaussian") != "gaussian":
@@ -418,6 +424,7 @@ class Controller:
         self.noise_source = noise_source
         self.device = int(device)
         self.stream = stream
+        self.group_width = int(group_width)
         self.last_diagnostics = None
         self._base = None
         self._dev = None   # created lazily: no CUDA before a fork (sim.py:321-322)
@@ -445,7 +452,8 @@ class Controller:
             M = cfg.inner_samples if cfg.kind == "bss" else 1
             prob, keep = build_problem(cfg.kind, cfg.samples, cfg.horizon, M, cfg.temperature,
                                        cfg.control_cost_weight, cfg.sigma_eps, cfg.precision,
-                                       cfg.bounds, cfg.persist_particles, self.ctx, k0, kn)
+                                       cfg.bounds, cfg.persist_particles, self.ctx, k0, kn,
+                                       group_width=self.group_width)
             self._dev = DeviceContext(prob, self.device, self.stream)
             del keep
         return self._dev
@@ -545,6 +553,14 @@ class Controller:
                                                        _lib.C.c_void_p(out.data_ptr())))
         self.iteration += 1
         return out
+
+    def launch_shape(self):
+        """(lanes per rollout, threads per block) of this controller's
+        rollout kernel (bssmppi_launch_shape)."""
+        dev = self._device_ctx()
+        g, b = _lib.C.c_int32(), _lib.C.c_int32()
+        _lib.check(dev.lib.bssmppi_launch_shape(dev.h, _lib.C.byref(g), _lib.C.byref(b)))
+        return g.value, b.value
 
     def download(self):
         """Synchronise; (v+ (T,2), diagnostics dict) of the last iteration."""

@@ -77,7 +77,11 @@ struct bssmppi_ctx {
   double *h_out = nullptr;    // pinned, mapped: final update kernels write v+ and head here
   double *h_out_dev = nullptr;  // device alias of h_out
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evr = nullptr;   // iteration start/end, rollout end
+  cudaEvent_t ev_h2d = nullptr;   // last h_state -> d_state copy (h_state reuse guard)
+  bool h2d_pending = false;
   bool timed = false;
+  int sms = 148;                  // multiprocessors of the device (launch-shape policy)
+  int force_g = 0;                // bssmppi_problem.group_width (0 = policy)
 };
 
 namespace {
@@ -95,6 +99,8 @@ struct DeviceGuard {
 
 constexpr size_t kSmemMax = 227 * 1024;   // opt-in dynamic shared memory per block
 constexpr int kPersistMaxM = 1792;         // persist clouds of one G = 32 block fit kSmemMax
+
+bool valid_group_width(int g) { return g == 2 || g == 4 || g == 8 || g == 16 || g == 32; }
 
 int validate(const bssmppi_problem *p) {
   if (!p) return fail(BSSMPPI_ERR_INVALID, "problem is NULL");
@@ -125,6 +131,8 @@ int validate(const bssmppi_problem *p) {
   if (!(p->dt > 0.0)) return fail(BSSMPPI_ERR_INVALID, "dt must be > 0");
   if (p->noise_kind < 0 || p->noise_kind > 1) return fail(BSSMPPI_ERR_INVALID, "unknown noise kind %d", p->noise_kind);
   if (p->n_obstacles < 0 || p->n_obstacles > 64) return fail(BSSMPPI_ERR_UNSUPPORTED, "0..64 obstacles supported");
+  if (p->group_width != 0 && !valid_group_width(p->group_width))
+    return fail(BSSMPPI_ERR_INVALID, "group_width must be 0 (policy) or 2, 4, 8, 16, 32 (got %d)", p->group_width);
   if (p->n_obstacles > 0 && (!p->obstacles || !p->centerline || p->centerline_n < 2 || !(p->centerline_ds > 0.0)))
     return fail(BSSMPPI_ERR_INVALID, "obstacles need a centerline table");
   return BSSMPPI_OK;
@@ -265,21 +273,10 @@ void fill_params(bssmppi_ctx *c, const bssmppi_problem *p) {
 // or a tied G on every one.  Decided on the LOCAL rollout count, so a
 // K-shard of 2048 rollouts (C3 over 8 GPUs) keeps one warp per rollout;
 // across world sizes the moment sums may then differ by FP32 summation order.
-#ifndef BSS_BIG_MIN_WARPS
-#define BSS_BIG_MIN_WARPS 1900
-#endif
-#ifndef BSS_BIG_MAX_WARPS
-#define BSS_BIG_MAX_WARPS 2368
-#endif
-constexpr long long kBigBlockMinWarps = BSS_BIG_MIN_WARPS;   // 512-thread blocks for
-constexpr long long kBigBlockMaxWarps = BSS_BIG_MAX_WARPS;   // [min, max] warps per launch
+// bssmppi_problem.group_width pins G explicitly (parity tests at the
+// production widths, sweeps).
 
 int group_width(int M, int K) {
-  static const int forced = [] {   // tuning override (tools/g_sweep.py); 0 = policy
-    const char *e = std::getenv("BSSMPPI_FORCE_G");
-    return e ? std::atoi(e) : 0;
-  }();
-  if (forced == 2 || forced == 4 || forced == 8 || forced == 16 || forced == 32) return forced;
   int g = 2;
   while (g < M && g < 32) g <<= 1;
   const auto warps = [K](int gg) { return (long long)K * gg / 32; };
@@ -295,34 +292,44 @@ size_t persist_smem(int g, int M) {
          (size_t)(kBlockThreads / g) * 8 * M * sizeof(float);
 }
 
-int rollout_group_width(int M, int K, bool persist) {
-  int g = group_width(M, K);
+// forced: bssmppi_problem.group_width (0 = the policy above).
+int rollout_group_width(int M, int K, bool persist, int forced = 0) {
+  int g = forced ? forced : group_width(M, K);
   while (persist && g < 32 && persist_smem(g, M) > kSmemMax) g <<= 1;
   return g;
 }
 
 // Block size of the belief kernel: 128 threads (4 blocks per SM) in
 // general; 512 (one block per SM, same registers and occupancy) when the
-// launch is one nearly full wave (1900-2368 warps): the 8-GPU shards of C3
-// and C4 and the C2 control step ran 4-5% faster that way, while 1024-warp
+// launch is one nearly full wave -- between 80% and 100% of
+// (SMs x 16 warps), 1900-2368 warps on 148 SMs: the 8-GPU shards of C3 and
+// C4 and the C2 control step ran 4-5% faster that way, while half-wave
 // launches (half the SMs left idle with 512-thread blocks) and multi-wave
 // ones ran slower (tools/block_sweep.sh, profiles/r1_block_sweep.txt).
-// BSSMPPI_FORCE_BLOCK overrides (sweeps).
-int rollout_block_threads(int k_count, int G, bool persist, bool zarr) {
+// BSSMPPI_FORCE_BLOCK = 128 | 512 overrides (sweeps); other values are
+// reported and ignored.
+#ifndef BSS_BIG_MIN_FRAC
+#define BSS_BIG_MIN_FRAC 0.8
+#endif
+int rollout_block_threads(int k_count, int G, bool persist, bool zarr, int sms) {
   static const int forced = [] {
     const char *e = std::getenv("BSSMPPI_FORCE_BLOCK");
-    return e ? std::atoi(e) : 0;
+    const int v = e ? std::atoi(e) : 0;
+    if (e && v != kBlockThreads && v != kMaxBlockThreads)
+      std::fprintf(stderr, "bssmppi: BSSMPPI_FORCE_BLOCK=%s ignored (128 or 512)\n", e);
+    return (v == kBlockThreads || v == kMaxBlockThreads) ? v : 0;
   }();
   // persist: clouds sized per 128-thread block; zarr (parity runs): 128 only
   if (persist || zarr) return kBlockThreads;
-  if (forced == kBlockThreads || forced == kMaxBlockThreads) return forced;
+  if (forced) return forced;
   const long long warps = (long long)k_count * G / 32;
-  return (warps >= kBigBlockMinWarps && warps <= kBigBlockMaxWarps) ? kMaxBlockThreads : kBlockThreads;
+  const long long wave = (long long)sms * (kBlockThreads / 32) * BSS_MIN_BLOCKS;
+  return (warps >= (long long)(BSS_BIG_MIN_FRAC * wave) && warps <= wave) ? kMaxBlockThreads : kBlockThreads;
 }
 
 template <int G>
-cudaError_t launch_bss_g(const RollParams &rp, bool persist, bool zarr, cudaStream_t st) {
-  const int threads = rollout_block_threads(rp.k_count, G, persist, zarr);
+cudaError_t launch_bss_g(const RollParams &rp, bool persist, bool zarr, int sms, cudaStream_t st) {
+  const int threads = rollout_block_threads(rp.k_count, G, persist, zarr, sms);
   const int GPB = threads / G;   // rollouts per block
   const int blocks = (rp.k_count + GPB - 1) / GPB;
   size_t smem = (size_t)(threads / 32) * (32 / G) * 2 * kSlotFloats * sizeof(float);
@@ -343,12 +350,12 @@ cudaError_t launch_bss_g(const RollParams &rp, bool persist, bool zarr, cudaStre
 int launch_rollout(bssmppi_ctx *c, const RollParams &rp, bool zarr) {
   cudaError_t e;
   if (c->kind == BSSMPPI_KIND_BSS) {
-    switch (rollout_group_width(rp.M, rp.k_count, c->persist != 0)) {
-      case 2: e = launch_bss_g<2>(rp, c->persist, zarr, c->stream); break;
-      case 4: e = launch_bss_g<4>(rp, c->persist, zarr, c->stream); break;
-      case 8: e = launch_bss_g<8>(rp, c->persist, zarr, c->stream); break;
-      case 16: e = launch_bss_g<16>(rp, c->persist, zarr, c->stream); break;
-      default: e = launch_bss_g<32>(rp, c->persist, zarr, c->stream); break;
+    switch (rollout_group_width(rp.M, rp.k_count, c->persist != 0, c->force_g)) {
+      case 2: e = launch_bss_g<2>(rp, c->persist, zarr, c->sms, c->stream); break;
+      case 4: e = launch_bss_g<4>(rp, c->persist, zarr, c->sms, c->stream); break;
+      case 8: e = launch_bss_g<8>(rp, c->persist, zarr, c->sms, c->stream); break;
+      case 16: e = launch_bss_g<16>(rp, c->persist, zarr, c->sms, c->stream); break;
+      default: e = launch_bss_g<32>(rp, c->persist, zarr, c->sms, c->stream); break;
     }
   } else {
     const int blocks = (rp.k_count + kBlockThreads - 1) / kBlockThreads;
@@ -396,10 +403,15 @@ int ensure(T **p, size_t *cap, size_t n) {
 int stage_state(bssmppi_ctx *c, const double *x0, const double *cov0, const double *plan) {
   if (!x0 || !plan) return fail(BSSMPPI_ERR_INVALID, "x0 and plan are required");
   float *h = c->h_state;
+  // the previous upload's asynchronous copy may still be queued behind an
+  // iteration: wait for it before rewriting the pinned staging buffer
+  if (c->h2d_pending) CUDA_TRY(cudaEventSynchronize(c->ev_h2d));
   for (int i = 0; i < 8; ++i) h[i] = (float)x0[i];
   for (int i = 0; i < 16; ++i) h[8 + i] = cov0 ? (float)cov0[i] : 0.f;
   for (int i = 0; i < 2 * c->T; ++i) h[24 + i] = (float)plan[i];
   CUDA_TRY(cudaMemcpyAsync(c->d_state, h, (24 + 2 * c->T) * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaEventRecord(c->ev_h2d, c->stream));
+  c->h2d_pending = true;
   return BSSMPPI_OK;
 }
 
@@ -496,6 +508,18 @@ int32_t bssmppi_group_width(int32_t inner_samples, int32_t k_count) {
   return group_width(std::max(2, inner_samples), std::max(1, k_count));
 }
 
+int32_t bssmppi_launch_shape(const bssmppi_ctx *c, int32_t *group_width_out, int32_t *block_threads_out) {
+  if (!c) return fail(BSSMPPI_ERR_INVALID, "ctx is NULL");
+  int g = 1, bt = kBlockThreads;
+  if (c->kind == BSSMPPI_KIND_BSS) {
+    g = rollout_group_width(c->M, c->k_count, c->persist != 0, c->force_g);
+    bt = rollout_block_threads(c->k_count, g, c->persist != 0, false, c->sms);
+  }
+  if (group_width_out) *group_width_out = g;
+  if (block_threads_out) *block_threads_out = bt;
+  return BSSMPPI_OK;
+}
+
 int bssmppi_create(const bssmppi_problem *problem, int32_t device, bssmppi_ctx **out) {
   if (!out) return fail(BSSMPPI_ERR_INVALID, "out is NULL");
   *out = nullptr;
@@ -517,6 +541,8 @@ int bssmppi_create(const bssmppi_problem *problem, int32_t device, bssmppi_ctx *
   c->k_count = problem->k_count;
   c->persist = problem->kind == BSSMPPI_KIND_BSS && problem->persist_particles;
   c->lam = problem->temperature;
+  c->force_g = problem->group_width;
+  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
   for (int i = 0; i < 2; ++i) { c->lo[i] = problem->bounds_lo[i]; c->hi[i] = problem->bounds_hi[i]; }
   fill_params(c, problem);
   auto bail = [&](int code) { bssmppi_destroy(c); return code; };
@@ -538,7 +564,8 @@ int bssmppi_create(const bssmppi_problem *problem, int32_t device, bssmppi_ctx *
       cudaHostGetDevicePointer((void **)&c->h_out_dev, c->h_out, 0) != cudaSuccess)
     return bail(fail(BSSMPPI_ERR_CUDA, "cudaMallocHost failed"));
   if (cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
-      cudaEventCreate(&c->evr) != cudaSuccess)
+      cudaEventCreate(&c->evr) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_h2d, cudaEventDisableTiming) != cudaSuccess)
     return bail(fail(BSSMPPI_ERR_CUDA, "cudaEventCreate failed"));
   CUDA_TRY(cudaMemset(c->d_state, 0, (24 + T2) * sizeof(float)));
   *out = c;
@@ -557,6 +584,7 @@ void bssmppi_destroy(bssmppi_ctx *c) {
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->evr) cudaEventDestroy(c->evr);
+  if (c->ev_h2d) cudaEventDestroy(c->ev_h2d);
   delete c;
 }
 
@@ -574,6 +602,8 @@ int bssmppi_upload_state(bssmppi_ctx *c, const double *x0, const double *cov0, c
 
 int bssmppi_enqueue_iteration(bssmppi_ctx *c, const uint32_t key_ctrl[2], const uint32_t key_belief[2]) {
   if (!c) return fail(BSSMPPI_ERR_INVALID, "ctx is NULL");
+  if (c->k_begin != 0 || c->k_count != c->K)
+    return fail(BSSMPPI_ERR_INVALID, "sharded context: use bssmppi_enqueue_partials + bssmppi_enqueue_combine");
   DeviceGuard guard(c->device);
   RollParams rp = iteration_params(c, key_ctrl, key_belief);
   return run_iteration(c, rp, true, nullptr);

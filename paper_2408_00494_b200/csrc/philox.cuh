@@ -103,13 +103,6 @@ __device__ __forceinline__ void box_muller_raw(uint32_t a, uint32_t b, float &z0
   z1 = r * s;
 }
 
-// Single raw normal (cosine branch) of a pair.
-__device__ __forceinline__ void box_muller_raw1(uint32_t a, uint32_t b, float &z0) {
-  const float u1 = 2.0f - __uint_as_float(0x3f800000u | (a >> 9));
-  const float ang = __uint_as_float(0x3f800000u | (b >> 9)) * 6.28318530718f;
-  z0 = sqrt_approx(-lg2_approx(u1)) * __cosf(ang);
-}
-
 // Standard normal pair (the oracle's bm()).
 __device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float &z0, float &z1) {
   box_muller_raw(a, b, z0, z1);
@@ -117,58 +110,87 @@ __device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float &z0, fl
   z1 *= kBmNeg;
 }
 
-// The 7 standard normals of particle-step (t, k, m) (Philox4x32-7 counters): [0:4] re-projection
-// on the tracked subset, [4:7] process noise -- the column layout of the
-// reference's z_all block (controllers.py:285-287, belief.py:328-333).
-// The two Philox4x32-7 blocks of particle-step (t, k, m); both noise kinds
-// (Gaussian, config-4 Laplace) transform the same eight words.
-__device__ __forceinline__ void belief_bits(const PhiloxKeys &rk, uint32_t t, uint32_t kg, uint32_t m,
-                                            Philox4 &a, Philox4 &b) {
-  a = philox4x32<kBeliefRounds>(Philox4{t, m, kg, 0u}, rk);
-  b = philox4x32<kBeliefRounds>(Philox4{t, m, kg, 1u}, rk);
+// Belief stream: ONE Philox4x32-7 block per particle-step (t, k, m), counter
+// (t, m, k_global, 0).  Each of its four words carries one Box-Muller pair:
+// the radius uniform from the word's top 20 bits, the angle from its low 12
+// bits (independent bit fields, so the pair stays an exact polar draw):
+//   u1 = 1 - (n + 1/2) 2^-20, n = w >> 12 (midpoint grid, never 0 or 1);
+//   theta = 2 pi j / 4096, j = w & 0xfff.
+// A 4096-point angle grid reproduces E[cos^p theta] exactly for every
+// p < 4096, so all low-order moments of the pair are those of the
+// continuous draw; the 20-bit radius truncates |z| at 5.3 sigma (tail mass
+// 1.2e-7).  Words 0..3 -> normals (z0, z1), (z2, z3), (z4, z5), (z6, -):
+// [0:4] re-projection on the tracked subset, [4:7] process noise -- the
+// column layout of the reference's z_all block (controllers.py:285-287,
+// belief.py:328-333).  One block instead of two halves the quarter-rate
+// IMAD.WIDE work per particle-step (profiles/README.md).
+constexpr float kU1Mid = 1.99999952316284180f;   // 2 - 2^-21 (exact in FP32)
+
+// Raw pair (standard / kBmNeg) of one word: -sqrt(-2 ln u1) (cos, sin)
+// theta = kBmNeg sqrt(-log2 u1) (cos, sin)(2 pi m_a), m_a = 1 + j / 4096.
+__device__ __forceinline__ float word_radius(uint32_t w) {
+  // 1 + n 2^-20 by bit insertion (mask, then one LEA.HI), then the exact
+  // Sterbenz difference (2 - 2^-21) - (1 + n 2^-20)
+  const float u1 = kU1Mid - __uint_as_float(0x3f800000u + ((w & 0xfffff000u) >> 9));
+  return sqrt_approx(-lg2_approx(u1));
+}
+__device__ __forceinline__ float word_angle(uint32_t w) {
+  return __uint_as_float(0x3f800000u | ((w & 0xfffu) << 11)) * 6.28318530718f;
+}
+__device__ __forceinline__ void box_muller_word(uint32_t w, float &z0, float &z1) {
+  const float r = word_radius(w);
+  float s, c;
+  __sincosf(word_angle(w), &s, &c);
+  z0 = r * c;
+  z1 = r * s;
+}
+__device__ __forceinline__ void box_muller_word1(uint32_t w, float &z0) {
+  z0 = word_radius(w) * __cosf(word_angle(w));
+}
+
+__device__ __forceinline__ Philox4 belief_block(const PhiloxKeys &rk, uint32_t t, uint32_t kg, uint32_t m) {
+  return philox4x32<kBeliefRounds>(Philox4{t, m, kg, 0u}, rk);
 }
 
 // The 7 raw normals (standard normals / kBmNeg) of a particle-step.
-__device__ __forceinline__ void raw_normals_from_bits(const Philox4 &a, const Philox4 &b, float z[7]) {
-  box_muller_raw(a.x, a.y, z[0], z[1]);
-  box_muller_raw(a.z, a.w, z[2], z[3]);
-  box_muller_raw(b.x, b.y, z[4], z[5]);
-  box_muller_raw1(b.z, b.w, z[6]);
+__device__ __forceinline__ void raw_normals_from_block(const Philox4 &a, float z[7]) {
+  box_muller_word(a.x, z[0], z[1]);
+  box_muller_word(a.y, z[2], z[3]);
+  box_muller_word(a.z, z[4], z[5]);
+  box_muller_word1(a.w, z[6]);
 }
 
 // The 7 standard normals of particle-step (t, k, m) (statistics / parity kernel).
 __device__ __forceinline__ void belief_normals(const PhiloxKeys &rk, uint32_t t, uint32_t kg,
                                                uint32_t m, float z[7]) {
-  Philox4 a, b;
-  belief_bits(rk, t, kg, m, a, b);
-  raw_normals_from_bits(a, b, z);
+  raw_normals_from_block(belief_block(rk, t, kg, m), z);
 #pragma unroll
   for (int j = 0; j < 7; ++j) z[j] *= kBmNeg;
 }
 
-// Config-4 extension: 4 re-projection normals + Laplace(0, b) on (vx, vy, r)
-// + U(-a, a) lateral slip on vy from the same two Philox4x32-7 blocks (the
-// second block's words become the uniforms instead of Box-Muller normals).
-// 2u for the centred uniform u = (n + 1/2) 2^-23 - 1/2 of the top 23 bits n
-// of w, i.e. (2n + 1 - 2^23) 2^-23 in (-1, 1): the mantissa m = 1 + n 2^-23
-// by bit insertion, 2m - 3 (exact FFMA), + 2^-23 (exact) -- no I2F.
-__device__ __forceinline__ float centred_uniform2(uint32_t w) {
-  return fmaf(__uint_as_float(0x3f800000u | (w >> 9)), 2.0f, -3.0f) + 1.1920928955078125e-07f;
+// Config-4 extension from the same single block: 4 re-projection normals
+// (words 0, 1 as above) + Laplace(0, b) on (vx, vy, r) + U(-a, a) lateral
+// slip on vy from the four 16-bit halves of words 2, 3.
+// 2u for the centred uniform u = (n + 1/2) 2^-16 - 1/2 of a 16-bit field n,
+// i.e. (2n + 1 - 2^16) 2^-16 in (-1, 1): the mantissa m = 1 + n 2^-16 by bit
+// insertion, 2m - 3 (exact FFMA), + 2^-16 (exact) -- no I2F.
+__device__ __forceinline__ float centred_uniform2_16(uint32_t field_at_top) {
+  // field_at_top: the 16-bit field in bits 16..31, zeros below
+  return fmaf(__uint_as_float(0x3f800000u + (field_at_top >> 9)), 2.0f, -3.0f) + 1.52587890625e-05f;
 }
 
 // z[0:4] are RAW normals (x kBmNeg = standard), w the noise increments.
-__device__ __forceinline__ void laplace_from_bits(const Philox4 &p, const Philox4 &q, float b, float a,
-                                                  float z[4], float w[3]) {
-  box_muller_raw(p.x, p.y, z[0], z[1]);
-  box_muller_raw(p.z, p.w, z[2], z[3]);
-  const uint32_t words[3] = {q.x, q.y, q.z};
+__device__ __forceinline__ void laplace_from_block(const Philox4 &p, float b, float a, float z[4], float w[3]) {
+  box_muller_word(p.x, z[0], z[1]);
+  box_muller_word(p.y, z[2], z[3]);
+  const uint32_t fields[4] = {p.z & 0xffff0000u, p.z << 16, p.w & 0xffff0000u, p.w << 16};
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    const float v = centred_uniform2(words[i]);   // 2u
+    const float v = centred_uniform2_16(fields[i]);   // 2u
     // inverse CDF: -b sgn(u) ln(1 - 2|u|)
     w[i] = -b * copysignf(0.69314718056f * lg2_approx(1.0f - fabsf(v)), v);
   }
-  w[1] += a * centred_uniform2(q.w);             // U(-a, a) = 2a u
+  w[1] += a * centred_uniform2_16(fields[3]);          // U(-a, a) = 2a u
 }
 
 // The 2 standard normals of control sample (k, t) (controllers.py:175).

@@ -10,7 +10,8 @@
 //     (<= 32) narrowed by the measured policy in bssmppi.cu group_width
 //     (C3: G = 8, 4 rollouts per warp, 32 particles per lane); no
 //     block-level sync exists at all;
-//   * particles never touch memory: noise, re-projection x = mu + L z, the
+//   * particles never touch memory: noise (one Philox4x32-7 block per
+//     particle-step, philox.cuh), re-projection x = mu + L z, the
 //     Euler step, process noise and the moment sums all stay in registers;
 //     the noise of particle m + G is generated inside particle m's
 //     iteration (software pipelining, particle_pass);
@@ -375,10 +376,9 @@ __device__ __forceinline__ void particle_noise(const RollParams &P, int t, int k
       for (int j = 0; j < 7; ++j) n[j] = 0.f;
     }
   } else {
-    Philox4 a, b;
-    belief_bits(P.kb, (uint32_t)t, (uint32_t)kg, (uint32_t)m, a, b);
-    if (NK == NK_LAPLACE) laplace_from_bits(a, b, P.lap_b, P.slip_a, n, n + 4);
-    else raw_normals_from_bits(a, b, n);
+    const Philox4 a = belief_block(P.kb, (uint32_t)t, (uint32_t)kg, (uint32_t)m);
+    if (NK == NK_LAPLACE) laplace_from_block(a, P.lap_b, P.slip_a, n, n + 4);
+    else raw_normals_from_block(a, n);
   }
 }
 

@@ -196,9 +196,10 @@ combine_kernel(int nrec, int T2, const double *rec, double lam, int final_, doub
     if (!final_) {
       rec_out[kRecHead + col] = a;
     } else {
+      // no finite rollout (AllRolloutsInvalid): v+ is NaN, never a clamped 0/0
       const double v = a / s_head[1];
       const double l = (col & 1) ? lo1 : lo0, h = (col & 1) ? hi1 : hi0;
-      vplus[col] = fmin(fmax(v, l), h);
+      vplus[col] = s_head[3] > 0.0 ? fmin(fmax(v, l), h) : __longlong_as_double(0x7ff8000000000000ll);
       if (mirror != nullptr) mirror[col] = vplus[col];
     }
   }
@@ -210,7 +211,9 @@ combine_kernel(int nrec, int T2, const double *rec, double lam, int final_, doub
       if (mirror != nullptr) mirror[T2 + tid] = s_head[tid];
     }
   }
-  if (final_ && plan_out != nullptr) {
+  // AllRolloutsInvalid leaves the warm start untouched (the reference raises
+  // before replacing the plan, controllers.py:183-185, 407-409)
+  if (final_ && plan_out != nullptr && s_head[3] > 0.0) {
     __syncthreads();
     for (int col = tid; col < T2; col += kCombThreads) {
       const int src = (col + 2 < T2) ? col + 2 : col;   // drop first, repeat last
@@ -303,14 +306,14 @@ update_small_kernel(int n, int k_begin, int T2, const float *costs, const float 
     for (int sl = 0; sl < ns; ++sl) a += s_part[sl * T2 + col];
     const double v = a / s_head[1];
     const double l = (col & 1) ? lo1 : lo0, h = (col & 1) ? hi1 : hi0;
-    vplus[col] = fmin(fmax(v, l), h);
+    vplus[col] = nfin > 0.0 ? fmin(fmax(v, l), h) : __longlong_as_double(0x7ff8000000000000ll);
     if (mirror != nullptr) mirror[col] = vplus[col];
   }
   if (tid < kRecHead) {
     head_out[tid] = s_head[tid];
     if (mirror != nullptr) mirror[T2 + tid] = s_head[tid];
   }
-  if (plan_out != nullptr) {
+  if (plan_out != nullptr && nfin > 0.0) {   // AllRolloutsInvalid: plan untouched
     __syncthreads();
     for (int col = tid; col < T2; col += kCombThreads) {
       const int src = (col + 2 < T2) ? col + 2 : col;   // drop first, repeat last

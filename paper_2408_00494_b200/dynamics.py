@@ -36,10 +36,6 @@ DEFAULT_NOISE_CHANNELS = (IDX_VX, IDX_VY, IDX_YAW_RATE)
 _DEFAULT_PEAK = 0.7 * 22.0 * G / 2.0
 
 
-class CurvilinearSingularity(RuntimeError):
-    """State left the road-aligned frame validity region (1 - kappa*e_y <= 0)."""
-
-
 class OpenLoop(ValueError):
     """Track segment list does not close the loop."""
 
@@ -136,15 +132,6 @@ class VehicleState:
         (reference dynamics.py:131-135)."""
         omega = vx / params.wheel_radius
         return cls(vx=vx, omega_f=omega, omega_r=omega, **kwargs)
-
-
-@dataclass
-class ControlInput:
-    delta: float = 0.0
-    throttle: float = 0.0
-
-    def as_array(self):
-        return np.array([self.delta, self.throttle], dtype=float)
 
 
 def _loop_turn(s, kappa, length, closed):
@@ -294,7 +281,3 @@ class NoiseModel:
     @property
     def is_zero(self):
         return not np.any(self.cov)
-
-
-def wrap_angle(angle):
-    return np.pi - np.mod(np.pi - angle, 2.0 * np.pi)

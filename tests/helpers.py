@@ -71,6 +71,35 @@ class Inputs:
 COV_FLOOR = 1e-24   # sigma^2 of 1e-12: below it a variance is rounding noise
 
 
+def unpack_moments(mom):
+    """(..., 18) device/C-oracle layout -> mean (..., 8), cov (..., 4, 4)."""
+    mean = np.asarray(mom[..., :8], dtype=np.float64)
+    up = np.asarray(mom[..., 8:], dtype=np.float64)
+    cov = np.empty(mean.shape[:-1] + (4, 4))
+    q = 0
+    for a in range(4):
+        for b in range(a, 4):
+            cov[..., a, b] = cov[..., b, a] = up[..., q]
+            q += 1
+    return mean, cov
+
+
+def moments_err_arrays(mean_a, cov_a, mean_b, cov_b):
+    """Elementwise SURVEY 8c moment errors: (em (..., 8), ec (..., 4, 4))."""
+    sub = [1, 2, 5, 6]
+    sig = np.sqrt(np.clip(np.diagonal(cov_b, axis1=-2, axis2=-1), 0, None))
+    scale_m = np.abs(mean_b).copy()
+    scale_m[..., sub] = np.maximum(scale_m[..., sub], sig)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        em = np.abs(mean_a - mean_b) / scale_m
+        em = np.where(scale_m == 0, np.where(mean_a == mean_b, 0.0, np.inf), em)
+        var = np.maximum(sig ** 2, COV_FLOOR)
+        denom = np.sqrt(np.einsum("...i,...j->...ij", var, var))
+        ec = np.abs(cov_a - cov_b) / denom
+        ec = np.where(denom == 0, np.where(cov_a == cov_b, 0.0, np.inf), ec)
+    return em, ec
+
+
 def moments_rel_err(mean_a, cov_a, mean_b, cov_b, floor=None):
     """SURVEY.md 8c moment metric: |dmu_i| / max(|mu_i|, sigma_i) over the
     tracked components (sigma from b) and |dSigma_ab| / sqrt(S_aa S_bb).

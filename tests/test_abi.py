@@ -38,7 +38,7 @@ def test_binding_covers_header():
 
 def test_abi_version_and_record_length():
     lib = _lib.load()
-    assert lib.bssmppi_abi_version() == 2
+    assert lib.bssmppi_abi_version() == 3
     assert lib.bssmppi_partial_len(50) == 105
 
 

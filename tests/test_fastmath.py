@@ -2,6 +2,7 @@
 one in float32 with the kernel's Horner order and bound its error against
 float64 on the range the particle step uses."""
 
+import math
 import re
 from pathlib import Path
 
@@ -148,18 +149,40 @@ def test_sincos_pi_x2_half_range():
     assert (es[nz] / np.abs(np.sin(x64[nz]))).max() < 3e-7
 
 
-def test_centred_uniform2_is_exact():
-    """philox.cuh centred_uniform2: the I2F-free 2u (mantissa bit insertion,
-    FFMA 2m - 3, + 2^-23) equals 2 x the reference-form centred uniform
-    (n + 1/2) 2^-23 - 1/2 for every 23-bit n, and the derived Laplace
-    inputs 1 - |2u| and a (2u) are bit-identical to 1 - 2|u| and (2a) u."""
-    n = np.arange(0, 1 << 23, dtype=np.uint32)
-    m = (np.uint32(0x3F800000) | n).view(np.float32)
-    v = (m.astype(np.float64) * 2.0 - 3.0).astype(np.float32) + np.float32(2.0 ** -23)
-    assert np.array_equal((m.astype(np.float64) * 2.0 - 3.0), (m.astype(np.float64) * 2.0 - 3.0).astype(np.float32))
-    u = (n.astype(np.float32) + np.float32(0.5)) * np.float32(2.0 ** -23) - np.float32(0.5)
+def test_centred_uniform2_16_is_exact():
+    """philox.cuh centred_uniform2_16: the I2F-free 2u of a 16-bit field
+    (mantissa bit insertion, FFMA 2m - 3, + 2^-16) equals 2 x the
+    reference-form centred uniform (n + 1/2) 2^-16 - 1/2 for every n, and the
+    derived Laplace inputs 1 - |2u| and a (2u) are bit-identical to 1 - 2|u|
+    and (2a) u (oracle/bss_oracle.c centred_uniform16)."""
+    n = np.arange(0, 1 << 16, dtype=np.uint32)
+    top = n << np.uint32(16)                               # the field in bits 16..31
+    m = (np.uint32(0x3F800000) + (top >> np.uint32(9))).view(np.float32)
+    assert np.array_equal(m.astype(np.float64), 1.0 + n * 2.0 ** -16)
+    v = (m.astype(np.float64) * 2.0 - 3.0).astype(np.float32) + np.float32(2.0 ** -16)
+    u = (n.astype(np.float32) + np.float32(0.5)) * np.float32(2.0 ** -16) - np.float32(0.5)
     assert np.array_equal(v.astype(np.float64), 2.0 * u.astype(np.float64))
     assert np.abs(v).max() < 1.0
     assert np.array_equal(np.float32(1.0) - np.abs(v), np.float32(1.0) - np.float32(2.0) * np.abs(u))
     a = np.float32(0.05)
     assert np.array_equal(a * v, (np.float32(2.0) * a) * u)
+
+
+def test_word_uniforms_are_exact():
+    """philox.cuh word_radius / word_angle bit fields: the radius uniform
+    (2 - 2^-21) - (1 + n 2^-20) is exactly 1 - (n + 1/2) 2^-20 for every
+    20-bit n (Sterbenz), and the angle mantissa is exactly 1 + j / 4096 for
+    every 12-bit j -- the values oracle/bss_oracle.c bm_word uses in FP64."""
+    n = np.arange(0, 1 << 20, dtype=np.uint32)
+    w = n << np.uint32(12)
+    mr = (np.uint32(0x3F800000) + ((w & np.uint32(0xFFFFF000)) >> np.uint32(9))).view(np.float32)
+    u1 = np.float32(2.0 - 2.0 ** -21) - mr
+    assert np.array_equal(u1.astype(np.float64), 1.0 - (n + 0.5) * 2.0 ** -20)
+    assert u1.min() > 0 and u1.max() < 1
+    j = np.arange(0, 1 << 12, dtype=np.uint32)
+    ma = (np.uint32(0x3F800000) | ((j & np.uint32(0xFFF)) << np.uint32(11))).view(np.float32)
+    assert np.array_equal(ma.astype(np.float64), 1.0 + j / 4096.0)
+    # the 4096-point angle grid keeps the pair's low moments exact
+    th = 2 * np.pi * j / 4096.0
+    for p in (2, 4, 6):
+        assert abs(np.mean(np.cos(th) ** p) - math.comb(p, p // 2) / 2 ** p) < 1e-12

@@ -10,7 +10,10 @@ block is partial)."""
 import numpy as np
 import pytest
 
+from helpers import moments_err_arrays, unpack_moments
+
 from oracle import c_oracle
+from paper_2408_00494_b200 import _lib
 from paper_2408_00494_b200 import controllers as mc
 from paper_2408_00494_b200 import dynamics as md
 from paper_2408_00494_b200.tracks import named_track
@@ -34,11 +37,12 @@ def test_fullsize_philox_costs_and_update(K, M, T, dt):
     eps = rng.standard_normal((K, T, 2)) @ md.psd_factor(cfg.sigma_eps).T
     u = np.clip(nominal[None] + eps, [-0.35, -1.0], [0.35, 1.0])
     kb = (123456789, 987654321)
-    gpu = mc.rollout_bss(x0, np.zeros((4, 4)), mc.RolloutBatch(u, eps), nominal, ctx, mc.DeviceKey(kb), M,
-                         precision=cfg.precision, cost_weight=cfg.control_cost_weight)
+    gpu, gmom = mc.rollout_bss(x0, np.zeros((4, 4)), mc.RolloutBatch(u, eps), nominal, ctx, mc.DeviceKey(kb),
+                               M, precision=cfg.precision, cost_weight=cfg.control_cost_weight, moments=True)
     prob, keep = mc.build_problem("bss", K, T, M, 1.0, cfg.control_cost_weight, cfg.sigma_eps,
                                   cfg.precision, cfg.bounds, False, ctx)
-    ref, _ = c_oracle.rollout(prob, x0, np.zeros((4, 4)), nominal, u=u, eps=eps, key_belief=kb)
+    ref, _, rmom = c_oracle.rollout(prob, x0, np.zeros((4, 4)), nominal, u=u, eps=eps, key_belief=kb,
+                                    moments=True)
     fin = np.isfinite(ref)
     assert np.mean(np.isfinite(gpu) == fin) > 0.999
     both = fin & np.isfinite(gpu)
@@ -48,6 +52,17 @@ def test_fullsize_philox_costs_and_update(K, M, T, dt):
           f"all: frac<1e-3 {np.mean(rel < 1e-3):.5f}, median {np.median(rel):.1e}")
     assert np.max(np.abs(gpu[weighted] - ref[weighted]) / np.abs(ref[weighted])) < 1e-3
     assert np.mean(rel < 1e-3) > 0.99
+    # per-step belief moments at the production lane-group width (C3: G = 8,
+    # 32 particles per lane; C5 32768x64: G = 4, 16 per lane): the device's
+    # shifted one-pass sums vs the C oracle's tree mean + two-pass
+    # covariance (belief.py:275-308), on rollouts alive in both
+    G = _lib.load().bssmppi_group_width(M, K)
+    em, ec = moments_err_arrays(*unpack_moments(gmom), *unpack_moments(rmom))
+    per_k = np.maximum(em.max(axis=(0, 2)), ec.max(axis=(0, 2, 3)))
+    print(f"  G={G} ({-(-M // G)} particles per lane): moments max {per_k[weighted].max():.2e} (weighted), "
+          f"frac alive <= 1e-4 {np.mean(per_k[both] <= 1e-4):.5f}, median {np.median(per_k[both]):.1e}")
+    assert per_k[weighted].max() <= 1e-4
+    assert np.mean(per_k[both] <= 1e-4) > 0.99
     v_gpu = mc.mppi_update(mc.RolloutBatch(u, eps, gpu), 1.0, mc.ControlBounds()).controls
     v_ref = c_oracle.update(ref, u, 1.0, [-0.35, -1.0], [0.35, 1.0])
     top2 = np.sort(ref[fin])[:2]

@@ -40,7 +40,7 @@ def _near_tie(costs, lam, cost_err=1e-5):
     return fin.size > 1 and (fin[1] - fin[0]) < 10 * cost_err * abs(fin[0]) + 1e-9
 
 
-def _gpu_rollout(inp, moments=False):
+def _gpu_rollout(inp, moments=False, group_width=0):
     batch = mc.RolloutBatch(inp.u, inp.eps)
     if inp.kind == "bss":
         class _Z:
@@ -49,7 +49,8 @@ def _gpu_rollout(inp, moments=False):
                 return inp.z
         return mc.rollout_bss(inp.x0, inp.cov0, batch, inp.plan, inp.ctx, _Z(), inp.M,
                               precision=inp.cfg.precision, cost_weight=inp.cfg.control_cost_weight,
-                              persist_particles=inp.case["persist"], moments=moments)
+                              persist_particles=inp.case["persist"], moments=moments,
+                              group_width=group_width)
     fn = mc.rollout_smppi if inp.kind == "smppi" else mc.rollout_mppi
     return fn(inp.x0, batch, inp.plan, inp.ctx, precision=inp.cfg.precision,
               cost_weight=inp.cfg.control_cost_weight)

@@ -1,3 +1,3 @@
 for shape in "2048 256 50" "4096 256 50" "8192 256 50" "16384 256 50" "4096 128 40" "4096 64 60" "32768 64 60" "256 32 20" "4096 512 60" "8192 64 50"; do
-  for g in 4 8 16 32; do BSSMPPI_FORCE_G=$g timeout 120 python tools/g_sweep.py $shape 2>&1 | tail -1; done
+  for g in 4 8 16 32; do timeout 120 python tools/g_sweep.py $shape $g 2>&1 | tail -1; done
 done
