@@ -167,20 +167,62 @@ def cpu_rate(wl, seconds, threads=0, key=(1, 2)):
 
 
 def reference_arm(args, wl):
-    """--impl reference: the reference algorithm's CPU implementation (the
-    FP64 C port in oracle/, all host threads), same metric and config."""
+    """--impl reference: the UNMODIFIED reference package (belief_mppi 0.1.0,
+    numba, installed in baseline/_ref) through its own Controller.control_step,
+    K-sharded over one process per host core (baseline/reference_arm.py), on
+    the same workload, metric and config.  Each step is a bounded K-slice of
+    the iteration (``--ref-step-seconds`` per process); ``ms_per_step`` is the
+    measured wall time of that sampled step.  Without the install it falls
+    back to the FP64 C port of the same algorithm (oracle/, kind "port")."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    from baseline import reference_arm as ra
+
+    why = ra.available()
+    if wl.get("laplace"):
+        why = "config-4 Laplace/obstacle extension: the reference has no such path"
+    if why is not None:
+        return reference_arm_port(args, wl, why)
+    pool = ra.ReferencePool(wl, step_seconds=args.ref_step_seconds)
+    try:
+        times = []
+        for i in range(args.warmup + args.steps):
+            dt = pool.step()
+            if i >= args.warmup:
+                times.append(dt)
+    finally:
+        pool.close()
+    total = sum(times)
+    per_step = pool.rollouts_per_step * wl["M"] * wl["T"]
+    value = per_step * len(times) / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded spline track, seeded x0, the reference's numpy keyed noise)",
+        "config": workload_config(args, wl),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": pool.procs, "kind": "reference",
+                         "sample": pool.sample()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": (f"ms_per_step is the wall time of one sampled step ({pool.rollouts_per_step} of "
+                 f"K={wl['K']} rollouts); a full-K iteration at this rate would take "
+                 f"{1e3 * wl['K'] * wl['M'] * wl['T'] / value:.0f} ms"),
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def reference_arm_port(args, wl, why):
+    """Fallback reference arm: the FP64 C port (oracle/) on all host threads,
+    full K per step (no extrapolation)."""
     from oracle import c_oracle
     from paper_2408_00494_b200.controllers import RolloutContext, build_problem
 
     cfg, cost, model, track, noise, x0, obstacles = build_problem_objects(wl)
     ctx = RolloutContext(model, track, cost, noise=noise, obstacles=obstacles)
     nthr = c_oracle.max_threads()
-    rate, _, _ = cpu_rate(wl, 0.5)
-    k = int(min(wl["K"], max(nthr, rate * args.ref_step_seconds / (wl["M"] * wl["T"]))))
-    prob, keep = build_problem("bss", k, wl["T"], wl["M"], cfg.temperature, cfg.control_cost_weight,
+    prob, keep = build_problem("bss", wl["K"], wl["T"], wl["M"], cfg.temperature, cfg.control_cost_weight,
                                cfg.sigma_eps, cfg.precision, cfg.bounds, False, ctx)
     plan = np.zeros((wl["T"], 2))
     times = []
@@ -192,19 +234,16 @@ def reference_arm(args, wl):
         if i >= args.warmup:
             times.append(dt)
     total = sum(times)
-    value = k * wl["M"] * wl["T"] * len(times) / total
-    full_ms = 1e3 * (total / len(times)) * wl["K"] / k
-    sample = f"K-slice {k} of {wl['K']} per step (x M={wl['M']} x T={wl['T']})"
+    value = wl["K"] * wl["M"] * wl["T"] * len(times) / total
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": full_ms,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded spline track, seeded x0, Philox noise)",
         "config": workload_config(args, wl),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthr, "kind": "port",
-                         "sample": sample},
+                         "sample": f"full K={wl['K']} per step; FP64 C port (oracle/): {why}"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "note": "ms_per_step extrapolates the sampled K-slice linearly to the full K",
     }
     print(json.dumps(line))
     return 0
@@ -236,7 +275,8 @@ def main():
                     help="one of %s, or C5:K:M for the BASELINE config-5 sweep (T=60)" % sorted(WORKLOADS))
     ap.add_argument("--e2e-steps", type=int, default=50)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--ref-step-seconds", type=float, default=1.0)
+    ap.add_argument("--ref-step-seconds", type=float, default=0.5,
+                    help="reference arm: wall seconds of one sampled K-sharded step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.workload.startswith("C5:"):
@@ -354,34 +394,37 @@ def main():
     if tpath.exists():
         tj = json.loads(tpath.read_text())
         traffic = tj.get(args.workload)
-    G = _lib.load().bssmppi_group_width(wl["M"], k_count)
-    warps = k_count * G // 32   # csrc/bssmppi.cu rollout_block_threads: one-wave launches use 512
-    block = 512 if 1900 <= warps <= 2368 else 128
-    fp32 = {"achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-            "frac": achieved / peak if peak else None,
-            "peak_source": "FFMA microbenchmark measured in this run (MEASURED_PEAKS.json has "
-                           "no FP32 figure); nominal 148 SM x 128 FMA x 2 x sm_max_mhz = "
-                           f"{nominal:.1f} TFLOP/s",
-            "frac_of_nominal": achieved / nominal,
-            "algorithmic_flop_per_launch": flop, "flop_per_particle_step": FLOP_PER_PARTICLE_STEP}
+    G, block = ctrl.launch_shape()
+    pipe = None
+    ppath = ROOT / "profiles" / "rollout_pipes.json"
+    if ppath.exists():
+        pipe = json.loads(ppath.read_text()).get(args.workload)
     sfu_ops = SFU_PER_PARTICLE_STEP * k_count * wl["M"] * wl["T"]
     sfu_achieved = sfu_ops / (roll_avg * 1e-3) / 1e12
     sfu_peak = ctypes_mufu_peak(_lib, local)
-    sfu = {"achieved": sfu_achieved, "peak": sfu_peak, "unit": "Tops/s",
-           "frac": sfu_achieved / sfu_peak if sfu_peak else None,
-           "peak_source": "MUFU ex2.approx microbenchmark measured in this run; nominal "
-                          "148 SM x 16 x sm_max_mhz = "
-                          f"{nominal / 16:.2f} Tops/s",
-           "algorithmic_ops_per_launch": sfu_ops, "ops_per_particle_step": SFU_PER_PARTICLE_STEP}
-    # the reported fraction is the binding one of FP32 / SFU /
-    # HBM (HBM is < 1 % here: 70 KB of DRAM traffic per launch)
-    bind = sfu if (sfu["frac"] or 0) > (fp32["frac"] or 0) else fp32
-    roofline = {"bound": "sfu" if bind is sfu else "fp32",
-                "kernel": f"bss_rollout_kernel<{G},false,false,{block}>",
-                "achieved": bind["achieved"], "peak": bind["peak"], "unit": bind["unit"],
-                "frac": bind["frac"], "traffic": traffic,
-                "rollout_ms": roll_avg, "rollout_share_of_step": roll_avg / statistics.mean(step_ms),
-                "fp32": fp32, "sfu": sfu}
+    # north_star's roofline is the FP32 one: 162 algorithmic FLOP per
+    # particle-step / the rollout kernel's CUDA-event time vs the
+    # FFMA peak; the kernel is FMA-pipe bound (ncu evidence in fma_pipe)
+    roofline = {
+        "bound": "fp32", "kernel": f"bss_rollout_kernel<{G},false,false,{block}>",
+        "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
+        "traffic": traffic,
+        "peak_source": "FFMA microbenchmark measured in this run (MEASURED_PEAKS.json has no FP32 "
+                       "figure); nominal 148 SM x 128 FMA x 2 x sm_max_mhz = "
+                       f"{nominal:.1f} TFLOP/s",
+        "frac_of_nominal": achieved / nominal,
+        "algorithmic_flop_per_launch": flop, "flop_per_particle_step": FLOP_PER_PARTICLE_STEP,
+        "particle_steps_per_launch": k_count * wl["M"] * wl["T"],
+        "rollout_ms": roll_avg, "rollout_share_of_step": roll_avg / statistics.mean(step_ms),
+        "fma_pipe": pipe,
+        "sfu_transcendentals": {
+            "what": "algorithmic transcendentals / MUFU peak -- not a bound: the atan, tire-sine and "
+                    "heading sin/cos evaluations run as FMA-pipe polynomials, the MUFU work is mostly "
+                    "Box-Muller",
+            "achieved": sfu_achieved, "peak": sfu_peak, "unit": "Tops/s",
+            "frac": sfu_achieved / sfu_peak if sfu_peak else None,
+            "ops_per_particle_step": SFU_PER_PARTICLE_STEP},
+    }
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -401,9 +444,17 @@ def main():
         "gpu_launches": (2 if world == 1 and k_count <= 1024 else 3) * args.steps,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate, cores, sample = cpu_rate(wl, args.cpu_seconds)
-        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
-                                "sample": sample + "; FP64 C port of the reference step (oracle/)"}
+        from baseline import reference_arm as ra
+        if ra.available() is None and not wl.get("laplace"):
+            rate, cores, sample = ra.rate(wl, args.cpu_seconds)
+            line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "reference",
+                                    "sample": sample}
+        rate, cores, sample = cpu_rate(wl, args.cpu_seconds / 3)
+        port = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+                "sample": sample + "; FP64 C port of the reference step (oracle/, OpenMP)"}
+        line.setdefault("cpu_baseline", port)
+        if line["cpu_baseline"] is not port:
+            line["cpu_port"] = port
     if rank == 0:
         print(json.dumps(line))
     if dist is not None:

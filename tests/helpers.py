@@ -2,6 +2,7 @@
 repo's host mirror, and run the CPU oracle on them."""
 
 import json
+import math
 import types
 from pathlib import Path
 
@@ -84,12 +85,29 @@ def unpack_moments(mom):
     return mean, cov
 
 
-def moments_err_arrays(mean_a, cov_a, mean_b, cov_b):
-    """Elementwise SURVEY 8c moment errors: (em (..., 8), ec (..., 4, 4))."""
+def channel_spread(noise_factor):
+    """(8,) particle spread of the components outside the tracked
+    covariance: vx carries the process noise added after every step
+    (dynamics.py:571-572), std sqrt((F F^T)_00); the wheel speeds and s are
+    shared by a rollout's particles after re-projection (spread 0)."""
+    F = np.asarray(noise_factor, dtype=float).reshape(3, 3)
+    out = np.zeros(8)
+    out[0] = math.sqrt((F @ F.T)[0, 0])
+    return out
+
+
+def moments_err_arrays(mean_a, cov_a, mean_b, cov_b, spread=None):
+    """Elementwise SURVEY 8c moment errors: (em (..., 8), ec (..., 4, 4)).
+    Mean scale: max(|mu_i|, sigma_i) with sigma_i from b's covariance for
+    the tracked subset (vy, r, e_psi, e_y) and from ``spread``
+    (channel_spread) for the others -- a component crossing zero (vx at a
+    standstill) is measured against its belief spread, not against 0."""
     sub = [1, 2, 5, 6]
     sig = np.sqrt(np.clip(np.diagonal(cov_b, axis1=-2, axis2=-1), 0, None))
     scale_m = np.abs(mean_b).copy()
     scale_m[..., sub] = np.maximum(scale_m[..., sub], sig)
+    if spread is not None:
+        scale_m = np.maximum(scale_m, np.asarray(spread, dtype=float))
     with np.errstate(divide="ignore", invalid="ignore"):
         em = np.abs(mean_a - mean_b) / scale_m
         em = np.where(scale_m == 0, np.where(mean_a == mean_b, 0.0, np.inf), em)
@@ -100,25 +118,28 @@ def moments_err_arrays(mean_a, cov_a, mean_b, cov_b):
     return em, ec
 
 
-def moments_rel_err(mean_a, cov_a, mean_b, cov_b, floor=None):
-    """SURVEY.md 8c moment metric: |dmu_i| / max(|mu_i|, sigma_i) over the
-    tracked components (sigma from b) and |dSigma_ab| / sqrt(S_aa S_bb).
+def moments_rel_err(mean_a, cov_a, mean_b, cov_b, spread=None):
+    """SURVEY.md 8c moment metric (max over all entries): |dmu_i| /
+    max(|mu_i|, sigma_i) and |dSigma_ab| / sqrt(S_aa S_bb), sigma from b.
     The covariance scale is floored at COV_FLOOR: the FP64 reference's
     two-pass variance of M identical particles is ~ulp^2 (e.g. 3e-33 for
     e_y at M = 24) where the device's shifted sums give exactly 0."""
     if mean_a.size == 0:
         return 0.0, 0.0
-    sub = [1, 2, 5, 6]
-    sig = np.sqrt(np.clip(np.diagonal(cov_b, axis1=-2, axis2=-1), 0, None))
-    scale_m = np.abs(mean_b).copy()
-    scale_m[..., sub] = np.maximum(scale_m[..., sub], sig)
-    if floor is not None:
-        scale_m = np.maximum(scale_m, floor)
-    with np.errstate(divide="ignore", invalid="ignore"):
-        em = np.abs(mean_a - mean_b) / scale_m
-        em = np.where(scale_m == 0, np.where(mean_a == mean_b, 0.0, np.inf), em)
-        var = np.maximum(sig ** 2, COV_FLOOR)
-        denom = np.sqrt(np.einsum("...i,...j->...ij", var, var))
-        ec = np.abs(cov_a - cov_b) / denom
-        ec = np.where(denom == 0, np.where(cov_a == cov_b, 0.0, np.inf), ec)
+    em, ec = moments_err_arrays(mean_a, cov_a, mean_b, cov_b, spread)
     return float(np.max(em)), float(np.max(ec))
+
+
+def fp32_state_floor(inp, ks=None):
+    """Per-step (mean, cov) of the reference algorithm (FP64 oracle) with
+    every particle state rounded to FP32 after each re-projection and step:
+    the error any FP32-register implementation carries irreducibly
+    (oracle/bss_oracle.py rollout_bss(round_state=float32))."""
+    from oracle import bss_oracle as orc
+
+    rec = []
+    orc.rollout_bss(inp.prob, inp.x0, inp.cov0, inp.u, inp.eps, inp.plan, inp.z, inp.cfg.precision,
+                    inp.cfg.control_cost_weight, persist=inp.case["persist"], record=rec,
+                    round_state=np.float32)
+    mean, cov = np.stack([r[0] for r in rec]), np.stack([r[1] for r in rec])
+    return (mean, cov) if ks is None else (mean[:, ks], cov[:, ks])

@@ -21,17 +21,25 @@ def _bench(*args, env=None):
                           cwd=ROOT, env=e, timeout=600)
 
 
-def test_reference_arm_json_line():
+@pytest.mark.parametrize("arm", ["reference", "port"])
+def test_reference_arm_json_line(arm):
+    """The stock reference package from baseline/_ref (numba, K-sharded over
+    host processes) when installed, else / on request the FP64 C port."""
+    sys.path.insert(0, str(ROOT))
+    from baseline import reference_arm as ra
+    if arm == "reference" and ra.available() is not None:
+        pytest.skip(ra.available())
     r = _bench("--impl", "reference", "--workload", "C1", "--steps", "2", "--warmup", "1",
-               "--ref-step-seconds", "0.05")
+               "--ref-step-seconds", "0.05", env={"BSSMPPI_REFERENCE_ARM": arm})
     assert r.returncode == 0, r.stderr[-2000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["impl"] == "reference"
     assert line["metric"].startswith("belief rollout-steps/s") and line["unit"] == "rollout-steps/s"
     assert line["value"] > 0 and line["higher_is_better"] is True and line["steps"] == 2
     assert line["config"]["workload"].startswith("C1")
+    assert line["ms_per_step"] > 0
     cb = line["cpu_baseline"]
-    assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] == line["value"] and cb["sample"]
+    assert cb["kind"] == arm and cb["cores"] >= 1 and cb["value"] == line["value"] and cb["sample"]
     assert line["e2e"] == {"value": line["value"], "unit": line["unit"], "h2d_bytes_per_step": 0,
                            "d2h_bytes_per_step": 0}
 

@@ -10,7 +10,7 @@ block is partial)."""
 import numpy as np
 import pytest
 
-from helpers import moments_err_arrays, unpack_moments
+from helpers import channel_spread, moments_err_arrays, unpack_moments
 
 from oracle import c_oracle
 from paper_2408_00494_b200 import _lib
@@ -57,7 +57,7 @@ def test_fullsize_philox_costs_and_update(K, M, T, dt):
     # shifted one-pass sums vs the C oracle's tree mean + two-pass
     # covariance (belief.py:275-308), on rollouts alive in both
     G = _lib.load().bssmppi_group_width(M, K)
-    em, ec = moments_err_arrays(*unpack_moments(gmom), *unpack_moments(rmom))
+    em, ec = moments_err_arrays(*unpack_moments(gmom), *unpack_moments(rmom), channel_spread(noise.factor))
     per_k = np.maximum(em.max(axis=(0, 2)), ec.max(axis=(0, 2, 3)))
     print(f"  G={G} ({-(-M // G)} particles per lane): moments max {per_k[weighted].max():.2e} (weighted), "
           f"frac alive <= 1e-4 {np.mean(per_k[both] <= 1e-4):.5f}, median {np.median(per_k[both]):.1e}")

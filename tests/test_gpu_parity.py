@@ -14,7 +14,7 @@ import numpy as np
 import pytest
 
 from cases import CASES, UPDATE_BATCHES, update_batch
-from helpers import GOLDEN, Inputs, moments_rel_err
+from helpers import GOLDEN, Inputs, channel_spread, fp32_state_floor, moments_rel_err, unpack_moments
 
 from paper_2408_00494_b200 import controllers as mc
 
@@ -73,52 +73,53 @@ def test_rollout_costs(name):
         assert np.mean(rel < COST_RTOL) >= 0.99
 
 
-BRANCH_EDGE = {"s_wrap", "low_speed"}
+# Lane-group widths: 0 = the launch policy (G = 32 for every golden case),
+# 4 / 8 / 16 = the widths the BASELINE shapes run at (C3: G = 8, 32
+# particles per lane; C5 32768 x 64: G = 4; C2: G = 16), pinned through
+# bssmppi_problem.group_width so each lane pre-sums up to 64 particles of
+# the golden cases (M = 256 at G = 4).
+WIDTHS = (0, 4, 8, 16)
 
 
+def moment_tolerance(inp, ks, alive, spread):
+    """1e-4 (north_star), unless the reference's own algorithm with its
+    particle states held in FP32 (helpers.fp32_state_floor: FP64 arithmetic,
+    one FP32 rounding per state component per step) already errs by more
+    than half of that on this case; then 2x that floor.  The floor is
+    computed here, on the same inputs, so the exception is measured, not
+    asserted: it applies where particles straddle s = L (s_wrap, the belief
+    mean of wrapped arc lengths) and to the 4x4 sample covariance of M = 5
+    particles (ragged_m5), whose smallest Cholesky pivot is below FP32 state
+    resolution."""
+    fm, fc = fp32_state_floor(inp, ks)
+    gold = inp.gold
+    fem, fec = moments_rel_err(fm[alive], fc[alive], gold["means"][alive], gold["covs"][alive], spread)
+    return max(MOM_TOL, 2.0 * fem), max(MOM_TOL, 2.0 * fec), (fem, fec)
+
+
+@pytest.mark.parametrize("G", WIDTHS, ids=lambda g: f"G{g}")
 @pytest.mark.parametrize("name", BSS)
-def test_belief_moments(name):
+def test_belief_moments(name, G):
+    """Per-step belief moments (belief.py:275-308) vs the reference's, at the
+    policy width and pinned production widths; metric of SURVEY 8c with the
+    mean of vx measured against its process-noise spread
+    (helpers.channel_spread), no other floor."""
     inp = Inputs(name)
-    costs, mom = _gpu_rollout(inp, moments=True)
+    costs, mom = _gpu_rollout(inp, moments=True, group_width=G)
     gold = inp.gold
     ks = gold["ks"]
-    mean = mom[:, ks, :8].astype(np.float64)
-    up = mom[:, ks, 8:].astype(np.float64)
-    cov = np.empty(mean.shape[:2] + (4, 4))
-    q = 0
-    for a in range(4):
-        for b in range(a, 4):
-            cov[..., a, b] = cov[..., b, a] = up[..., q]
-            q += 1
+    mean, cov = unpack_moments(mom[:, ks])
     # compare rollouts that survive the horizon (a dead rollout is +inf and
     # weightless; its moments after leaving the curvilinear frame are
     # frame-singular in both implementations)
     alive = np.broadcast_to(np.isfinite(gold["costs"][ks])[None, :], mean.shape[:2])
-    # A degenerate belief (zero spread: sigma = 0) makes |dmu| / max(|mu|, sigma)
-    # ill-posed for components that pass near zero; floor the scale at 1e-2 of
-    # the component's own magnitude along the horizon.  (Exactness of the
-    # collapse itself is tested on the device: test_gpu_semantics.py.)
-    floor = 1e-2 * np.abs(gold["means"]).max(axis=0, keepdims=True)
-    em, ec = moments_rel_err(mean[alive], cov[alive], gold["means"][alive], gold["covs"][alive],
-                             floor=np.broadcast_to(floor, mean.shape)[alive])
+    spread = channel_spread(inp.noise.factor)
+    em, ec = moments_rel_err(mean[alive], cov[alive], gold["means"][alive], gold["covs"][alive], spread)
+    tol_m, tol_c, floor = moment_tolerance(inp, ks, alive, spread)
     zero = gold["covs"][alive] == 0.0
-    print(f"{name}: moments mean {em:.2e} cov {ec:.2e}")
-    # With M < 16 particles the 4x4 sample covariance is nearly singular
-    # (smallest Cholesky pivot ~1e-6 of the diagonal): its FP32 states
-    # resolve the deviations only to ~ulp(|x|)/sigma, so the downstream
-    # moments carry a conditioning floor of a few 1e-4.  All BASELINE
-    # configs use M >= 32.
-    tol = MOM_TOL if inp.M >= 16 else 5 * MOM_TOL
-    # Branch-edge regimes of the reference's own model, where FP32 rounding is
-    # amplified, not a device deviation (their costs still agree to ~1e-6):
-    # s_wrap -- particles straddling s = L enter the belief mean as ~0 and ~L
-    # (the reference's plain mean of wrapped arc lengths), so a last-bit
-    # difference decides which side a particle lands on; low_speed -- below
-    # the 0.3 m/s floor the explicit Euler longitudinal dynamics oscillate
-    # step to step (vx 0.02 <-> 0.4), amplifying a 1e-7 rounding to ~1e-5.
-    if name in BRANCH_EDGE:
-        tol = 10 * MOM_TOL
-    assert em <= tol and ec <= tol
+    print(f"{name} G={G}: moments mean {em:.2e} cov {ec:.2e} (tol {tol_m:.1e}/{tol_c:.1e}; "
+          f"fp32-state floor {floor[0]:.1e}/{floor[1]:.1e})")
+    assert em <= tol_m and ec <= tol_c
     assert np.all(cov[alive][zero] == 0.0), "exact zero covariances must stay zero"
 
 
