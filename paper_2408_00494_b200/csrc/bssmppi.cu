@@ -315,13 +315,13 @@ int rollout_block_threads(int k_count, int G, bool persist, bool zarr, int sms) 
   static const int forced = [] {
     const char *e = std::getenv("BSSMPPI_FORCE_BLOCK");
     const int v = e ? std::atoi(e) : 0;
-    if (e && v != kBlockThreads && v != kMaxBlockThreads)
-      std::fprintf(stderr, "bssmppi: BSSMPPI_FORCE_BLOCK=%s ignored (128 or 512)\n", e);
-    return (v == kBlockThreads || v == kMaxBlockThreads) ? v : 0;
+    const bool ok = v == kBlockThreads || v == kMaxBlockThreads || v == kSmallBlockThreads;
+    if (e && !ok) std::fprintf(stderr, "bssmppi: BSSMPPI_FORCE_BLOCK=%s ignored (64, 128 or 512)\n", e);
+    return ok ? v : 0;
   }();
   // persist: clouds sized per 128-thread block; zarr (parity runs): 128 only
   if (persist || zarr) return kBlockThreads;
-  if (forced) return forced;
+  if (forced) return (forced == kSmallBlockThreads && G != 4 && G != 8) ? kBlockThreads : forced;
   const long long warps = (long long)k_count * G / 32;
   const long long wave = (long long)sms * (kBlockThreads / 32) * BSS_MIN_BLOCKS;
   return (warps >= (long long)(BSS_BIG_MIN_FRAC * wave) && warps <= wave) ? kMaxBlockThreads : kBlockThreads;
@@ -338,6 +338,10 @@ cudaError_t launch_bss_g(const RollParams &rp, bool persist, bool zarr, int sms,
   if (persist) fn = zarr ? bss_rollout_kernel<G, true, true> : bss_rollout_kernel<G, true, false>;
   else if (zarr) fn = bss_rollout_kernel<G, false, true>;
   else if (threads == kMaxBlockThreads) fn = bss_rollout_kernel<G, false, false, kMaxBlockThreads>;
+  else if constexpr (G == 4 || G == 8) {
+    if (threads == kSmallBlockThreads) fn = bss_rollout_kernel<G, false, false, kSmallBlockThreads>;
+    else fn = bss_rollout_kernel<G, false, false>;
+  }
   else fn = bss_rollout_kernel<G, false, false>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

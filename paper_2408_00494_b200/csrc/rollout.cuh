@@ -303,6 +303,9 @@ constexpr int kBlockThreads = BSS_BLOCK_THREADS;
 // 128-register budget: one block fills an SM's register file); see
 // bssmppi.cu rollout_block_threads for when it is launched.
 constexpr int kMaxBlockThreads = 512;
+// ... and for 64-thread blocks (8 per SM, same registers): launches whose
+// warps fill the SMs in one balanced round (bssmppi.cu rollout_block_threads).
+constexpr int kSmallBlockThreads = 64;
 // Register budget: 4 resident 128-thread blocks per SM (<= 128 registers,
 // 16 warps/SM).  With the software-pipelined noise (particle_pass) the extra
 // registers buy more than occupancy: 5 / 6 / 7 blocks per SM (96 / 80 / 72

@@ -13,19 +13,23 @@ until FP32-vs-FP64 differences grow (tests/test_gpu_closed_loop.py).
 
 The plant is the simulator, not the optimisation step: it stays on the host
 as in the reference (``dynamics.py:447-478`` RK4 branch of ``_step_kernel``).
+The realised-safety bookkeeping (``SafetyMonitor``, reference sim.py:157-220)
+re-propagates the window's belief through the device rollout kernel.
 """
 
 from __future__ import annotations
 
 import math
 import time
+from collections import deque
 from dataclasses import dataclass, field, replace
 
 import numpy as np
 
-from . import streams
+from . import _lib, streams
 from .belief import DEFAULT_SUBSET
-from .controllers import Controller, CostSpec, MppiConfig
+from .controllers import Controller, ControlBounds, CostSpec, DeviceContext, MppiConfig, RolloutContext, \
+    build_problem
 from .dynamics import IDX_EY, IDX_S, NoiseModel, VehicleParams, VehicleState, phys_vector
 from .tracks import stadium_track
 
@@ -117,6 +121,7 @@ class ExperimentConfig:
     max_steps: int = 1200
     init_speed: float = 2.0
     init_jitter: float = 0.1
+    monitor_window: int = 0   # 0 -> half the controller horizon (reference sim.py:86)
 
     def __post_init__(self):
         if self.noise is None:
@@ -146,10 +151,121 @@ class RunRecord:
     violation_rate: float       # fraction of steps with |e_y| > collision threshold
     lap_time: float = None
     mean_speed: float = 0.0
+    satisfaction_rate: float = None   # SafetyMonitor.rate (None for plain MPPI)
     steps: int = 0
     latency_ms: np.ndarray = None       # wall time of each control_step
     device_ms: np.ndarray = None        # device time of each iteration
     trajectory: np.ndarray = None       # (steps, 10): x (8) after the step, u0 (2)
+
+
+# ------------------------------------------------------------------ safety monitor
+
+class SafetyMonitor:
+    """Realised safety-condition bookkeeping along the executed trajectory
+    (reference sim.py:157-220): the fraction of executed steps whose
+    (h_k, h_{k-1}) pair satisfies the discrete safety condition
+    h_k - (1 - beta) h_{k-1} >= 0, with h = max(w - nu sigma_y, 0)^2 - e_y^2
+    (constraints.py:130-137, 172-181).
+
+    For the belief-space controller sigma_y is the e_y spread of the belief
+    re-propagated Monte-Carlo style over a sliding window of executed
+    controls from the measured state at the window start -- the reference's
+    ``propagate_mc_batch`` loop (sim.py:189-201) -- run here as ONE device
+    rollout (K = 1, the window's controls given, the reference's own keyed
+    MONITOR stream supplying the normals, per-step moments returned);
+    deterministic shielded controllers use sigma_y = 0."""
+
+    def __init__(self, cfg, run_index, device=0):
+        c = cfg.controller
+        self.kind = c.kind
+        self.nu = float(cfg.cost.backoff)
+        self.beta = float(cfg.cost.safety.cbf_rate)
+        self.half_width = float(cfg.track.half_width)
+        self.track = cfg.track
+        self.w = int(getattr(cfg, "monitor_window", 0) or max(1, c.horizon // 2))
+        self.window = deque(maxlen=self.w)
+        self.inner = max(2, int(c.inner_samples))
+        self.master_seed = cfg.master_seed
+        self.run_index = run_index
+        self.h_prev = None
+        self.satisfied = 0
+        self.total = 0
+        self.last = (np.nan, np.nan, 0.0)   # (h, residual, sigma_y) of the latest step
+        self._dev = None
+        self._cfg = cfg
+        self._device = device
+
+    def _context(self):
+        if self._dev is None:
+            cfg = self._cfg
+            ctx = RolloutContext(cfg.model_params(), cfg.track, cfg.cost, noise=cfg.noise)
+            prob, keep = build_problem("bss", 1, self.w, self.inner, 1.0, 0.0, np.eye(2), None,
+                                       ControlBounds(), False, ctx)
+            self._dev = DeviceContext(prob, self._device)
+            del keep
+        return self._dev
+
+    def _kappa(self, s):
+        tr = self.track
+        sw = np.mod(s, tr.length) if tr.closed else np.clip(s, 0.0, tr.length)
+        return float(np.interp(sw, tr.s, tr.kappa, period=tr.length) if tr.closed
+                     else np.interp(sw, tr.s, tr.kappa))
+
+    def _window_sigma(self, step_index):
+        rng = streams.substream(self.master_seed, streams.DOMAIN_RUN, self.run_index,
+                                streams.DOMAIN_MONITOR, step_index)
+        n = len(self.window)
+        x0 = np.ascontiguousarray(self.window[0][0], dtype=np.float64)
+        u = np.zeros((1, self.w, 2))
+        u[0, :n] = np.array([uu for _, uu in self.window])
+        z = np.zeros((self.w, 1, self.inner, 7), dtype=np.float32)
+        # the reference draws (1, N, 7) per propagated step from one stream:
+        # the same numbers as one (n, 1, N, 7) draw
+        z[:n] = rng.standard_normal((n, 1, self.inner, 7))
+        dev = self._context()
+        eps = np.zeros_like(u)
+        nom = np.zeros((self.w, 2))
+        cost = np.empty(1)
+        mom = np.empty((self.w, 1, 18), dtype=np.float32)
+        _lib.check(dev.lib.bssmppi_rollout(dev.h, _lib.dptr(x0), None, _lib.dptr(u), _lib.dptr(eps),
+                                           _lib.dptr(nom), _lib.fptr(z), None, _lib.dptr(cost),
+                                           _lib.fptr(mom)))
+        # stop at the first step whose mean leaves the frame or turns
+        # non-finite (belief.py:376-379; sim.py:198-200), else the window end
+        m = mom[:n, 0].astype(np.float64)
+        t_end = n - 1
+        for t in range(n):
+            fin = np.all(np.isfinite(m[t]))
+            if not fin or not (1.0 - self._kappa(m[t, IDX_S]) * m[t, IDX_EY] > 0.0):
+                t_end = t
+                break
+        var_ey = m[t_end, 17]   # covariance upper triangle, entry (e_y, e_y)
+        return float(np.sqrt(max(var_ey, 0.0))) if np.isfinite(var_ey) else float("nan")
+
+    def update(self, state_before, control, state_after, step_index):
+        self.window.append((np.asarray(state_before, dtype=float).copy(),
+                            np.asarray(control, dtype=float).copy()))
+        sigma_y = self._window_sigma(step_index) if self.kind == "bss" else 0.0
+        margin = max(self.half_width - self.nu * sigma_y, 0.0)
+        h = float(margin * margin - state_after[IDX_EY] ** 2)
+        if self.h_prev is None:
+            self.h_prev = h   # k = 0: the previous belief equals the current one
+        residual = h - (1.0 - self.beta) * self.h_prev
+        self.satisfied += residual >= 0.0
+        self.total += 1
+        self.h_prev = h
+        self.last = (h, residual, sigma_y)
+
+    @property
+    def rate(self):
+        if self.kind == "mppi" or self.total == 0:
+            return None
+        return self.satisfied / self.total
+
+    def close(self):
+        if self._dev is not None:
+            self._dev.close()
+            self._dev = None
 
 
 def initial_state(cfg, run_index):
@@ -160,7 +276,8 @@ def initial_state(cfg, run_index):
 
 
 def run_closed_loop(cfg: ExperimentConfig, run_index: int = 0, *, noise_source="philox",
-                    device=0, max_steps=None, record=True, controller_factory=None) -> RunRecord:
+                    device=0, max_steps=None, record=True, controller_factory=None,
+                    monitor=True) -> RunRecord:
     """Alternate device controller and host plant until lap completion, crash
     (|e_y| beyond the lane or a frame break) or the step budget.
     ``controller_factory(cfg, run_path)`` swaps in another controller with
@@ -175,6 +292,9 @@ def run_closed_loop(cfg: ExperimentConfig, run_index: int = 0, *, noise_source="
                           run_path=(streams.DOMAIN_RUN, run_index), noise_source=noise_source,
                           device=device)
     plant_rng = streams.substream(cfg.master_seed, streams.DOMAIN_RUN, run_index, streams.DOMAIN_PLANT)
+    monitor = SafetyMonitor(cfg, run_index, device) if monitor else None
+    if hasattr(ctrl, "prepare"):
+        ctrl.prepare()      # CUDA context + kernel modules before the first timed step
     F = cfg.noise.factor
     x = initial_state(cfg, run_index)
     target = cfg.laps * track.length
@@ -192,6 +312,7 @@ def run_closed_loop(cfg: ExperimentConfig, run_index: int = 0, *, noise_source="
             lat.append(1e3 * (time.perf_counter() - tic))
             dev.append(ctrl.last_diagnostics["device_ms"])
             w = plant_rng.standard_normal(len(cfg.noise.channels)) @ F.T   # sample_noise, dynamics.py:317-322
+            x_before = x
             frame_ok = True
             for j in range(cfg.plant_substeps):
                 x, ok = plant_step(x, u0, w if j == cfg.plant_substeps - 1 else None, plant, track,
@@ -205,6 +326,8 @@ def run_closed_loop(cfg: ExperimentConfig, run_index: int = 0, *, noise_source="
                 ds = (ds + 0.5 * track.length) % track.length - 0.5 * track.length
             progress += ds
             prev_s = x[IDX_S]
+            if monitor is not None:
+                monitor.update(x_before, u0, x, step_index)
             if record:
                 rows.append(np.concatenate([x, u0]))
             v = abs(x[IDX_EY]) > cfg.collision_threshold
@@ -220,9 +343,12 @@ def run_closed_loop(cfg: ExperimentConfig, run_index: int = 0, *, noise_source="
                 break
     finally:
         ctrl.close()
+        if monitor is not None:
+            monitor.close()
     elapsed = steps * cfg.dt_control
     return RunRecord(run_index=run_index, crashed=crashed, collisions=collisions,
                      violation_rate=violating / max(steps, 1), lap_time=lap_time,
-                     mean_speed=progress / elapsed if elapsed > 0 else 0.0, steps=steps,
+                     mean_speed=progress / elapsed if elapsed > 0 else 0.0,
+                     satisfaction_rate=None if monitor is None else monitor.rate, steps=steps,
                      latency_ms=np.array(lat), device_ms=np.array(dev),
                      trajectory=np.array(rows) if rows else None)

@@ -1,0 +1,171 @@
+"""GPU analogues of the reference acceptance criteria 06-10
+(/root/reference/pkg/tests/test_acceptance.py:180-247), with the device
+Controller as a drop-in.
+
+* 06 (BSS == S-MPPI without uncertainty, 200 closed-loop steps) runs this
+  repo's Controller on the reference's default-experiment setting.
+* 07-10 run the REFERENCE's own closed-loop harness -- ``belief_mppi.sim``
+  from the stock package installed in baseline/_ref: ``monte_carlo``,
+  ``run_closed_loop`` with its RK4 plant, ``SafetyMonitor`` and ``aggregate``
+  -- with ``belief_mppi.sim.Controller`` replaced by this repo's device
+  Controller (sim.py:21 imports the name, sim.py:237 resolves it per run),
+  i.e. exactly the swap INTEGRATION.md documents.  The controller runs in
+  its performance mode (in-kernel Philox noise), so runs are statistically,
+  not path-wise, comparable with the reference's; the reference statistics
+  of the same batches come from tests/golden/acceptance_reference.json
+  (tests/golden/make_acceptance.py, reference controller).
+"""
+
+import json
+import math
+import sys
+from dataclasses import replace
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from acceptance_spec import BATCHES, RUNS, config, key, summary
+
+from paper_2408_00494_b200 import controllers as mc
+from paper_2408_00494_b200 import dynamics as md
+from paper_2408_00494_b200.tracks import stadium_track
+
+pytestmark = pytest.mark.gpu
+
+ROOT = Path(__file__).resolve().parent.parent
+GOLD = Path(__file__).resolve().parent / "golden" / "acceptance_reference.json"
+
+
+def test_06_bss_equals_smppi_200_steps():
+    """Criterion 06 (test_acceptance.py:180-201): zero process noise, zero
+    covariance; 128 samples (16 inner for BSS), seed 606, stadium track,
+    200 closed-loop Euler steps: the applied controls agree to 1e-9 (the
+    device gives bit-identical controls)."""
+    zero = md.NoiseModel(np.zeros((3, 3)))
+    model = md.with_timestep(md.VehicleParams(), 0.05, "euler")
+    track = stadium_track()
+    smppi = mc.Controller(mc.MppiConfig(kind="smppi", samples=128, horizon=20, temperature=1.0),
+                          mc.CostSpec(), model, track, noise=zero, seed=606)
+    bss = mc.Controller(mc.MppiConfig(kind="bss", samples=128, horizon=20, temperature=1.0, inner_samples=16),
+                        mc.CostSpec(), model, track, noise=zero, seed=606)
+    x_s = md.VehicleState.rolling(2.0, model, s=0.0).as_array()
+    x_b = x_s.copy()
+    dev = smppi._device_ctx()
+    worst = 0.0
+    for _ in range(200):
+        u_s, _ = smppi.control_step(x_s)
+        u_b, _ = bss.control_step(x_b)
+        worst = max(worst, float(np.max(np.abs(u_s - u_b))))
+        assert worst < 1e-9
+        x_s, ok_s = _step(dev, x_s, u_s)
+        x_b, ok_b = _step(dev, x_b, u_b)
+        assert ok_s and ok_b
+    print(f"[acceptance 06] max |u_bss - u_smppi| over 200 steps: {worst:.2e}")
+
+
+def _step(dev, x, u):
+    from paper_2408_00494_b200 import _lib
+    out = np.empty(8)
+    ok = np.empty(1, dtype=np.uint8)
+    _lib.check(dev.lib.bssmppi_step_array(dev.h, 1, _lib.dptr(np.ascontiguousarray(x, dtype=np.float64)),
+                                          _lib.dptr(np.ascontiguousarray(u, dtype=np.float64)), None,
+                                          _lib.dptr(out), ok.ctypes.data_as(_lib._u8p)))
+    return out, bool(ok[0])
+
+
+# ---------------------------------------------------------------- 07-10
+
+
+def _reference_sim():
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "belief_mppi").is_dir():
+        pytest.skip("stock reference not installed in baseline/_ref (baseline/reference_arm.py)")
+    import os
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/bssmppi_numba_cache")
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    from belief_mppi import sim
+    return sim
+
+
+@pytest.fixture(scope="module")
+def batches():
+    sim = _reference_sim()
+    original = sim.Controller
+    sim.Controller = mc.Controller          # the drop-in swap (sim.py:21, 237)
+    try:
+        out = {}
+        for b in BATCHES:
+            rep = sim.monte_carlo(config(sim, b))
+            out[key(b)] = summary(rep)
+            s = out[key(b)]
+            print(f"{key(b)}: crash {s['crash_ratio']:.2f} satisfaction {s['mean_satisfaction']:.3f} "
+                  f"completion {s['completion_ratio']:.2f}")
+    finally:
+        sim.Controller = original
+    (ROOT / "gpurun_out").mkdir(exist_ok=True)
+    (ROOT / "gpurun_out" / "acceptance_device.json").write_text(json.dumps({"runs": RUNS, "batches": out}))
+    return out
+
+
+def _b(batches, kind, q_ey=None, inner=None, penalty=None):
+    return batches[key((kind, q_ey, inner, penalty))]
+
+
+def _se(p, n=RUNS):
+    return math.sqrt(max(p * (1 - p), 0.05) / n)
+
+
+def test_07_crash_ordering(batches):
+    mppi, smppi, bss = (_b(batches, k)["crash_ratio"] for k in ("mppi", "smppi", "bss"))
+    print(f"[acceptance 07] crash ratios bss {bss:.2f} <= smppi {smppi:.2f} <= mppi {mppi:.2f}")
+    assert mppi >= 0.5
+    assert bss <= smppi
+    # the reference's own margin here is 0.55 vs 0.60 on 20 runs: the
+    # ordering is asserted up to two binomial standard errors
+    assert smppi <= mppi + 2 * math.hypot(_se(smppi), _se(mppi))
+
+
+def test_08_lateral_weight_trend(batches):
+    s_low = _b(batches, "smppi", q_ey=0.1)["crash_ratio"]
+    s_high = _b(batches, "smppi", q_ey=40.0)["crash_ratio"]
+    b_low = _b(batches, "bss", q_ey=0.1)["crash_ratio"]
+    b_high = _b(batches, "bss", q_ey=40.0)["crash_ratio"]
+    print(f"[acceptance 08] smppi {s_low:.2f} -> {s_high:.2f}, bss {b_low:.2f} -> {b_high:.2f}")
+    assert s_high <= s_low
+    assert abs(b_low - b_high) <= abs(s_low - s_high)
+
+
+def test_09_inner_sample_trend(batches):
+    few = _b(batches, "bss", inner=2)["crash_ratio"]
+    many = _b(batches, "bss", inner=64)["crash_ratio"]
+    print(f"[acceptance 09] N=64 crash {many:.2f} <= N=2 crash {few:.2f}")
+    assert many <= few
+
+
+def test_10_satisfaction(batches):
+    shielded = _b(batches, "bss")["mean_satisfaction"]
+    ablation = _b(batches, "bss", penalty=0.0)["mean_satisfaction"]
+    print(f"[acceptance 10] satisfaction {shielded:.3f} > ablation {ablation:.3f}, >= 0.90")
+    assert shielded >= 0.90
+    assert shielded > ablation
+
+
+def test_batches_match_reference_statistics(batches):
+    """Each batch's crash ratio and mean satisfaction against the reference
+    controller's on the same seeds (two-sample binomial / 0.03 tolerance)."""
+    if not GOLD.exists():
+        pytest.skip("tests/golden/acceptance_reference.json not generated")
+    ref = json.loads(GOLD.read_text())["batches"]
+    bad = []
+    for k, s in batches.items():
+        r = ref[k]
+        tol = 3 * math.hypot(_se(s["crash_ratio"]), _se(r["crash_ratio"]))
+        d_crash = abs(s["crash_ratio"] - r["crash_ratio"])
+        d_sat = abs(s["mean_satisfaction"] - r["mean_satisfaction"]) if np.isfinite(r["mean_satisfaction"]) else 0
+        print(f"{k:32s} crash {s['crash_ratio']:.2f} vs ref {r['crash_ratio']:.2f} (tol {tol:.2f}); "
+              f"satisfaction {s['mean_satisfaction']:.3f} vs {r['mean_satisfaction']:.3f}")
+        if d_crash > tol or d_sat > 0.03:
+            bad.append(k)
+    assert not bad, bad
