@@ -335,6 +335,11 @@ cudaError_t launch_bss_g(const RollParams &rp, bool persist, bool zarr, int sms,
   size_t smem = (size_t)(threads / 32) * (32 / G) * 2 * kSlotFloats * sizeof(float);
   if (persist) smem += (size_t)GPB * 8 * rp.M * sizeof(float);
   void (*fn)(const RollParams);
+#ifdef BSS_AB_ONLY   // quick A/B builds: Philox re-projection kernels only
+  if (persist || zarr) return cudaErrorNotSupported;
+  fn = threads == kMaxBlockThreads ? bss_rollout_kernel<G, false, false, kMaxBlockThreads>
+                                   : bss_rollout_kernel<G, false, false>;
+#else
   if (persist) fn = zarr ? bss_rollout_kernel<G, true, true> : bss_rollout_kernel<G, true, false>;
   else if (zarr) fn = bss_rollout_kernel<G, false, true>;
   else if (threads == kMaxBlockThreads) fn = bss_rollout_kernel<G, false, false, kMaxBlockThreads>;
@@ -343,7 +348,11 @@ cudaError_t launch_bss_g(const RollParams &rp, bool persist, bool zarr, int sms,
     else fn = bss_rollout_kernel<G, false, false>;
   }
   else fn = bss_rollout_kernel<G, false, false>;
-  if (smem > 48 * 1024) {
+#endif
+  // the Philox kernels also hold the 32 KB Box-Muller angle table (static):
+  // past 48 KB in total the dynamic part needs the opt-in attribute
+  const size_t static_smem = (persist || zarr) ? 0 : (size_t)kAngleTab * sizeof(float2);
+  if (smem + static_smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }

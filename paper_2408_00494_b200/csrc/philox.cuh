@@ -134,36 +134,134 @@ __device__ __forceinline__ float word_radius(uint32_t w) {
   const float u1 = kU1Mid - __uint_as_float(0x3f800000u + ((w & 0xfffff000u) >> 9));
   return sqrt_approx(-lg2_approx(u1));
 }
-__device__ __forceinline__ float word_angle(uint32_t w) {
-  return __uint_as_float(0x3f800000u | ((w & 0xfffu) << 11)) * 6.28318530718f;
-}
-__device__ __forceinline__ void box_muller_word(uint32_t w, float &z0, float &z1) {
-  const float r = word_radius(w);
+// Angle grid (cos, sin)(2 pi j / 4096) = sincospi(j / 2048), j = w & 0xfff:
+// an exact-argument FP32 sincospif (<= 1 ulp), identical whether it is read
+// from a block's shared-memory table or evaluated in place.  The rollout
+// kernels tabulate the 4096 entries once per block (32 KB) and look the
+// pair up with one LDS.64: no MUFU.SIN / MUFU.COS and no angle arithmetic
+// per normal pair, and an error of 1 ulp instead of MUFU's 2^-21.4 absolute.
+constexpr int kAngleTab = 4096;
+__device__ __forceinline__ float2 angle_entry(uint32_t j) {
   float s, c;
-  __sincosf(word_angle(w), &s, &c);
-  z0 = r * c;
-  z1 = r * s;
-}
-__device__ __forceinline__ void box_muller_word1(uint32_t w, float &z0) {
-  z0 = word_radius(w) * __cosf(word_angle(w));
+  sincospif((float)j * (1.0f / 2048.0f), &s, &c);
+  return make_float2(c, s);
 }
 
-__device__ __forceinline__ Philox4 belief_block(const PhiloxKeys &rk, uint32_t t, uint32_t kg, uint32_t m) {
+// TAB: read the block's shared-memory table, else evaluate in place
+// (statistics kernel, persist mode).
+// The table of a rollout block (filled by bss_rollout_kernel; kernels that
+// never name it do not allocate it).  Indexed through the symbol, so the
+// LDS carries its offset as an immediate.
+__shared__ __align__(16) float2 g_angle_tab[kAngleTab];
+
+template <bool TAB>
+__device__ __forceinline__ float2 angle_cs(uint32_t w) {
+  if (TAB) return g_angle_tab[w & 0xfffu];
+  return angle_entry(w & 0xfffu);
+}
+
+template <bool TAB>
+__device__ __forceinline__ void box_muller_word(uint32_t w, float &z0, float &z1) {
+  const float r = word_radius(w);
+  const float2 cs = angle_cs<TAB>(w);
+  const float2 z = __fmul2_rn(make_float2(r, r), cs);
+  z0 = z.x;
+  z1 = z.y;
+}
+template <bool TAB>
+__device__ __forceinline__ void box_muller_word1(uint32_t w, float &z0) {
+  z0 = word_radius(w) * (TAB ? g_angle_tab[w & 0xfffu].x : angle_entry(w & 0xfffu).x);
+}
+
+__host__ __device__ __forceinline__ Philox4 belief_block(const PhiloxKeys &rk, uint32_t t, uint32_t kg, uint32_t m) {
   return philox4x32<kBeliefRounds>(Philox4{t, m, kg, 0u}, rk);
 }
 
-// The 7 raw normals (standard normals / kBmNeg) of a particle-step.
+// The same block split at the particle index.  In the counter (t, m, kg, 0)
+// only the y word depends on m, and y first meets a multiplier in round 1
+// (via x1 = hi(M1 kg) ^ m ^ k0).  So of the first three rounds' six
+// products, four -- M0 t, M1 kg (round 0), M1 z1 (round 1), M0 x2 (round 2)
+// -- are the same for every particle of a rollout step: `belief_prefix`
+// computes them once per (k, t), folded with their round keys into five
+// words, and `belief_block_m` finishes a particle's block with the
+// remaining 2 + 2 (R - 3) products (10 IMAD.WIDE instead of 14 at R = 7).
+// The words are bit-identical to belief_block (tests/test_philox_split_cpu.py).
+struct BeliefPrefix {
+  uint32_t c1;    // hi(M1 kg) ^ k0:          x1 = c1 ^ m
+  uint32_t w1k;   // lo(M0 t) ^ k3:           z2 = hi(M0 x1) ^ w1k
+  uint32_t y2k;   // lo(M1 z1) ^ k4:          x3 = hi(M1 z2) ^ y2k
+  uint32_t e;     // hi(M0 x2) ^ k5:          z3 = e ^ lo(M0 x1)
+  uint32_t w3;    // lo(M0 x2)
+};
+
+__host__ __device__ __forceinline__ BeliefPrefix belief_prefix(const PhiloxKeys &rk, uint32_t t, uint32_t kg) {
+  static_assert(kBeliefRounds >= 3, "belief_prefix hoists rounds 0-2");
+  uint32_t a_hi, a_lo, b_hi, b_lo, d_hi, d_lo, e_hi, e_lo;
+  mulhilo32(0xD2511F53u, t, a_hi, a_lo);
+  mulhilo32(0xCD9E8D57u, kg, b_hi, b_lo);
+  const uint32_t z1 = a_hi ^ rk.k[1];                 // w0 = 0
+  mulhilo32(0xCD9E8D57u, z1, d_hi, d_lo);
+  const uint32_t x2 = d_hi ^ b_lo ^ rk.k[2];          // y1 = lo(M1 kg)
+  mulhilo32(0xD2511F53u, x2, e_hi, e_lo);
+  return BeliefPrefix{b_hi ^ rk.k[0], a_lo ^ rk.k[3], d_lo ^ rk.k[4], e_hi ^ rk.k[5], e_lo};
+}
+
+__host__ __device__ __forceinline__ Philox4 belief_block_m(const BeliefPrefix &p, const PhiloxKeys &rk, uint32_t m) {
+  uint32_t c_hi, c_lo, f_hi, f_lo;
+  mulhilo32(0xD2511F53u, p.c1 ^ m, c_hi, c_lo);      // round 1, x1
+  const uint32_t z2 = c_hi ^ p.w1k;
+  mulhilo32(0xCD9E8D57u, z2, f_hi, f_lo);            // round 2, z2
+  Philox4 c{f_hi ^ p.y2k, f_lo, p.e ^ c_lo, p.w3};   // state after round 2
+#pragma unroll
+  for (int i = 3; i < kBeliefRounds; ++i) {
+    uint32_t hi0, lo0, hi1, lo1;
+    mulhilo32(0xD2511F53u, c.x, hi0, lo0);
+    mulhilo32(0xCD9E8D57u, c.z, hi1, lo1);
+    c = Philox4{hi1 ^ c.y ^ rk.k[2 * i], lo1, hi0 ^ c.w ^ rk.k[2 * i + 1], lo0};
+  }
+  return c;
+}
+
+// Radius mantissa 1 + n 2^-20 of a word (n = its top 20 bits): (w >> 9)
+// masked and OR-ed with the exponent in ONE three-input LOP3 -- the
+// exponent word comes from a register, since LOP3 takes one immediate.
+__device__ __forceinline__ float radius_mantissa(uint32_t w, uint32_t one_bits) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(w >> 9), "n"(0x7ffff8), "r"(one_bits));
+  return __uint_as_float(r);
+}
+
+// The 7 raw normals (standard normals / kBmNeg) of a particle-step: the
+// word_radius / box_muller_word arithmetic with the four uniforms formed
+// as two FADD2 pairs.
+template <bool TAB>
 __device__ __forceinline__ void raw_normals_from_block(const Philox4 &a, float z[7]) {
-  box_muller_word(a.x, z[0], z[1]);
-  box_muller_word(a.y, z[2], z[3]);
-  box_muller_word(a.z, z[4], z[5]);
-  box_muller_word1(a.w, z[6]);
+#ifdef __CUDA_ARCH__
+  uint32_t one;
+  asm("mov.b32 %0, 0x3f800000;" : "=r"(one));
+  const float2 u01 = __fadd2_rn(make_float2(kU1Mid, kU1Mid),
+                                make_float2(-radius_mantissa(a.x, one), -radius_mantissa(a.y, one)));
+  const float2 u23 = __fadd2_rn(make_float2(kU1Mid, kU1Mid),
+                                make_float2(-radius_mantissa(a.z, one), -radius_mantissa(a.w, one)));
+  const float r0 = sqrt_approx(-lg2_approx(u01.x)), r1 = sqrt_approx(-lg2_approx(u01.y));
+  const float r2 = sqrt_approx(-lg2_approx(u23.x)), r3 = sqrt_approx(-lg2_approx(u23.y));
+  const float2 p0 = __fmul2_rn(make_float2(r0, r0), angle_cs<TAB>(a.x));
+  const float2 p1 = __fmul2_rn(make_float2(r1, r1), angle_cs<TAB>(a.y));
+  const float2 p2 = __fmul2_rn(make_float2(r2, r2), angle_cs<TAB>(a.z));
+  z[0] = p0.x; z[1] = p0.y; z[2] = p1.x; z[3] = p1.y; z[4] = p2.x; z[5] = p2.y;
+  z[6] = r3 * (TAB ? g_angle_tab[a.w & 0xfffu].x : angle_entry(a.w & 0xfffu).x);
+#else
+  box_muller_word<TAB>(a.x, z[0], z[1]);
+  box_muller_word<TAB>(a.y, z[2], z[3]);
+  box_muller_word<TAB>(a.z, z[4], z[5]);
+  box_muller_word1<TAB>(a.w, z[6]);
+#endif
 }
 
 // The 7 standard normals of particle-step (t, k, m) (statistics / parity kernel).
 __device__ __forceinline__ void belief_normals(const PhiloxKeys &rk, uint32_t t, uint32_t kg,
                                                uint32_t m, float z[7]) {
-  raw_normals_from_block(belief_block(rk, t, kg, m), z);
+  raw_normals_from_block<false>(belief_block(rk, t, kg, m), z);
 #pragma unroll
   for (int j = 0; j < 7; ++j) z[j] *= kBmNeg;
 }
@@ -180,9 +278,10 @@ __device__ __forceinline__ float centred_uniform2_16(uint32_t field_at_top) {
 }
 
 // z[0:4] are RAW normals (x kBmNeg = standard), w the noise increments.
+template <bool TAB>
 __device__ __forceinline__ void laplace_from_block(const Philox4 &p, float b, float a, float z[4], float w[3]) {
-  box_muller_word(p.x, z[0], z[1]);
-  box_muller_word(p.y, z[2], z[3]);
+  box_muller_word<TAB>(p.x, z[0], z[1]);
+  box_muller_word<TAB>(p.y, z[2], z[3]);
   const uint32_t fields[4] = {p.z & 0xffff0000u, p.z << 16, p.w & 0xffff0000u, p.w << 16};
 #pragma unroll
   for (int i = 0; i < 3; ++i) {

@@ -8,8 +8,8 @@
 //   * one group of G lanes owns one rollout k and its M Monte-Carlo
 //     particles (lane l handles m = l, l+G, ...); G is the power of two >= M
 //     (<= 32) narrowed by the measured policy in bssmppi.cu group_width
-//     (C3: G = 8, 4 rollouts per warp, 32 particles per lane); no
-//     block-level sync exists at all;
+//     (C3: G = 8, 4 rollouts per warp, 32 particles per lane); the only
+//     block-level sync is the one after the Box-Muller angle table fill;
 //   * particles never touch memory: noise (one Philox4x32-7 block per
 //     particle-step, philox.cuh), re-projection x = mu + L z, the
 //     Euler step, process noise and the moment sums all stay in registers;
@@ -86,20 +86,25 @@ __device__ __forceinline__ float stage_cost(const float x[8], const RollParams &
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const float d = (i == 0) ? x[0] - P.v_goal : x[i];
-    acc = fmaf(P.q[i] * d, d, acc);
+    acc = fmaf(__fmul_rn(P.q[i], d), d, acc);
   }
   return acc + ((fabsf(x[6]) > P.tr.half_width) ? P.c_obs : 0.f);
 }
 
+// The cost terms below round every product and sum separately (__fmul_rn /
+// __fadd_rn cannot be contracted into FMAs): the belief and deterministic
+// kernels inline them into different code, and free contraction could then
+// round them differently -- BSS with a degenerate belief must reproduce
+// S-MPPI's costs bit for bit (acceptance criterion 06).
 __device__ __forceinline__ float dcbf(float ey, float sigy, const RollParams &P) {
   // constraints.py:130-137
-  const float margin = fmaxf(P.tr.half_width - P.nu * sigy, 0.f);
-  return margin * margin - ey * ey;
+  const float margin = fmaxf(__fsub_rn(P.tr.half_width, __fmul_rn(P.nu, sigy)), 0.f);
+  return __fsub_rn(__fmul_rn(margin, margin), __fmul_rn(ey, ey));
 }
 
 __device__ __forceinline__ float shield_penalty(float hc, float hp, const RollParams &P) {
   // constraints.py:172-186: C max(-(h_k - (1 - beta) h_{k-1}), 0)
-  return P.c_pen * fmaxf(-(hc - P.beta1 * hp), 0.f);
+  return __fmul_rn(P.c_pen, fmaxf(-__fsub_rn(hc, __fmul_rn(P.beta1, hp)), 0.f));
 }
 
 // Obstacle terms of a belief mean (config-4 extension, obstacles.py):
@@ -129,7 +134,7 @@ __device__ __forceinline__ float obstacle_terms(const RollParams &P, float s, fl
     const float d = d2 > 0.f ? d2 * inv : 0.f;
     inside |= d < o.z;
     const float eta = d2 > 0.f ? (dx * nx + dy * ny) * inv : 1.f;
-    h = fminf(h, d - o.z - P.nu_obs * fabsf(eta) * sigy);
+    h = fminf(h, __fsub_rn(__fsub_rn(d, o.z), __fmul_rn(__fmul_rn(P.nu_obs, fabsf(eta)), sigy)));
   }
   return h;
 }
@@ -166,7 +171,9 @@ __device__ __forceinline__ void control_at(const RollParams &P, int k, int kg, i
   }
   // gamma * v^T P (v + eps) with the UNCLAMPED v + eps (controllers.py:227)
   const float a0 = v0 + e0, a1 = v1 + e1;
-  ccost = P.gamma * (v0 * (P.prec[0] * a0 + P.prec[1] * a1) + v1 * (P.prec[2] * a0 + P.prec[3] * a1));
+  const float pa0 = __fadd_rn(__fmul_rn(P.prec[0], a0), __fmul_rn(P.prec[1], a1));
+  const float pa1 = __fadd_rn(__fmul_rn(P.prec[2], a0), __fmul_rn(P.prec[3], a1));
+  ccost = __fmul_rn(P.gamma, __fadd_rn(__fmul_rn(v0, pa0), __fmul_rn(v1, pa1)));
 }
 
 // sqrt(p) and 1/sqrt(p) of a positive pivot from one MUFU.RSQ (the non-ftz
@@ -366,8 +373,9 @@ enum NoiseKind { NK_GAUSS_DIAG = 0, NK_LAPLACE = 1, NK_GAUSS_GENERAL = 2 };
 // the reference's normals (guarded to zeros for m >= M).  NK, the noise
 // kind (NoiseKind), is a template parameter so that the pipelined loop body
 // of particle_pass is one branch-free scheduling region.
-template <bool ZARR, int NK>
-__device__ __forceinline__ void particle_noise(const RollParams &P, int t, int k, int kg, int m, float n[7]) {
+template <bool ZARR, int NK, bool TAB>
+__device__ __forceinline__ void particle_noise(const RollParams &P, const BeliefPrefix &bp,
+                                               int t, int k, int m, float n[7]) {
   if (ZARR) {
     if (m < P.M) {
       BSS_ASSERT(t < P.T && k < P.k_count);
@@ -379,9 +387,9 @@ __device__ __forceinline__ void particle_noise(const RollParams &P, int t, int k
       for (int j = 0; j < 7; ++j) n[j] = 0.f;
     }
   } else {
-    const Philox4 a = belief_block(P.kb, (uint32_t)t, (uint32_t)kg, (uint32_t)m);
-    if (NK == NK_LAPLACE) laplace_from_block(a, P.lap_b, P.slip_a, n, n + 4);
-    else raw_normals_from_block(a, n);
+    const Philox4 a = belief_block_m(bp, P.kb, (uint32_t)m);
+    if (NK == NK_LAPLACE) laplace_from_block<TAB>(a, P.lap_b, P.slip_a, n, n + 4);
+    else raw_normals_from_block<TAB>(a, n);
   }
 }
 
@@ -397,13 +405,20 @@ __device__ __forceinline__ void particle_step(const RollParams &P, int t, int m,
 #pragma unroll
     for (int i = 0; i < 8; ++i) x[i] = cloud[i * M + m];
   } else {
-    // x = mu, tracked subset (vy, r, e_psi, e_y) += L z[0:4] (belief.py:259-272)
+    // x = mu, tracked subset (vy, r, e_psi, e_y) += L z[0:4] (belief.py:259-272),
+    // as FP32x2 columns: (vy, r) += (L00, L10) z0, then r += L11 z1;
+    // (e_psi, e_y) += (L20, L30) z0 + (L21, L31) z1 + (L22, L32) z2, then
+    // e_y += L33 z3 -- 6 issue slots instead of 10
 #pragma unroll
     for (int i = 0; i < 8; ++i) x[i] = mean[i];
-    x[1] += L[0] * z[0];
-    x[2] += L[1] * z[0] + L[2] * z[1];
-    x[5] += L[3] * z[0] + L[4] * z[1] + L[5] * z[2];
-    x[6] += L[6] * z[0] + L[7] * z[1] + L[8] * z[2] + L[9] * z[3];
+    const float2 x12 = __ffma2_rn(bc2(z[0]), make_float2(L[0], L[1]), make_float2(mean[1], mean[2]));
+    float2 x56 = __ffma2_rn(bc2(z[0]), make_float2(L[3], L[6]), make_float2(mean[5], mean[6]));
+    x56 = __ffma2_rn(bc2(z[1]), make_float2(L[4], L[7]), x56);
+    x56 = __ffma2_rn(bc2(z[2]), make_float2(L[5], L[8]), x56);
+    x[1] = x12.x;
+    x[2] = fmaf(L[2], z[1], x12.y);
+    x[5] = x56.x;
+    x[6] = fmaf(L[9], z[3], x56.y);
   }
   // per-particle ok is discarded (belief.py:370); a re-projected particle
   // shares (vx, omega_f, omega_r, s) with the mean, hence the shared terms
@@ -415,8 +430,9 @@ __device__ __forceinline__ void particle_step(const RollParams &P, int t, int m,
     x[2] += z[6];
   } else if (NK == NK_GAUSS_DIAG) {      // added after integration (dynamics.py:571-572)
     x[0] = fmaf(F[0], z[4], x[0]);
-    x[1] = fmaf(F[4], z[5], x[1]);
-    x[2] = fmaf(F[8], z[6], x[2]);
+    const float2 x12 = __ffma2_rn(make_float2(F[4], F[8]), make_float2(z[5], z[6]), make_float2(x[1], x[2]));
+    x[1] = x12.x;
+    x[2] = x12.y;
   } else if (P.noise_on) {               // NK_GAUSS_GENERAL: 3x3 factor or none
     x[0] += F[0] * z[4] + F[1] * z[5] + F[2] * z[6];
     x[1] += F[3] * z[4] + F[4] * z[5] + F[5] * z[6];
@@ -448,6 +464,42 @@ __device__ __forceinline__ void accumulate(float acc[18], const float x[8], cons
   acc[16] = fmaf(a5, a6, acc[16]); acc[17] = fmaf(a6, a6, acc[17]);
 }
 
+// The same sums for re-projected particles (wheel sums identically zero) in
+// FP32x2 lanes: (S1_0, S1_7), (S1_1, S1_2), (S1_5, S1_6) and the products
+// (11, 22), (55, 66), (15, 16), (25, 26) as FADD2 / FFMA2, 12 and 56 scalar
+// -- 12 issue slots instead of 22, every lane rounded exactly like the
+// scalar form (bit-identical sums).
+struct AccPacked {
+  float2 a07, a12, a56, q1122, q5566, q1516, q2526;
+  float q12, q56;
+};
+
+// nc: the NEGATED shift pairs (-c0, -c7), (-c1, -c2), (-c5, -c6) (x - c
+// == x + (-c) exactly; there is no FSUB2).
+__device__ __forceinline__ void accumulate_packed(AccPacked &A, const float x[8], const float2 nc[3]) {
+  const float2 d07 = __fadd2_rn(make_float2(x[0], x[7]), nc[0]);
+  const float2 d12 = __fadd2_rn(make_float2(x[1], x[2]), nc[1]);
+  const float2 d56 = __fadd2_rn(make_float2(x[5], x[6]), nc[2]);
+  A.a07 = __fadd2_rn(A.a07, d07);
+  A.a12 = __fadd2_rn(A.a12, d12);
+  A.a56 = __fadd2_rn(A.a56, d56);
+  A.q1122 = __ffma2_rn(d12, d12, A.q1122);
+  A.q5566 = __ffma2_rn(d56, d56, A.q5566);
+  A.q1516 = __ffma2_rn(make_float2(d12.x, d12.x), d56, A.q1516);
+  A.q2526 = __ffma2_rn(make_float2(d12.y, d12.y), d56, A.q2526);
+  A.q12 = fmaf(d12.x, d12.y, A.q12);
+  A.q56 = fmaf(d56.x, d56.y, A.q56);
+}
+
+// Back to the acc[18] layout of group_allreduce18 / the moment formulas.
+__device__ __forceinline__ void unpack_acc(const AccPacked &A, float acc[18]) {
+  acc[0] = A.a07.x; acc[1] = A.a12.x; acc[2] = A.a12.y; acc[3] = 0.f; acc[4] = 0.f;
+  acc[5] = A.a56.x; acc[6] = A.a56.y; acc[7] = A.a07.y;
+  acc[8] = A.q1122.x; acc[9] = A.q12; acc[10] = A.q1516.x; acc[11] = A.q1516.y;
+  acc[12] = A.q1122.y; acc[13] = A.q2526.x; acc[14] = A.q2526.y; acc[15] = A.q5566.x;
+  acc[16] = A.q56; acc[17] = A.q5566.y;
+}
+
 // All particles of rollout k at step t for one lane (m = li, li + G, ...):
 // noise, step, and the shifted one-pass moment sums.  Particle 0 of the
 // group doubles as the shift c of the moments: it sits O(sigma) from the
@@ -460,17 +512,28 @@ __device__ __forceinline__ void accumulate(float acc[18], const float x[8], cons
 template <int G, bool PERSIST, bool ZARR, int NK, bool ST>
 __device__ __forceinline__ void particle_pass(const RollParams &P, int t, int k, int kg, int li,
                                               const float mean[8], const float L[10], const CtlDev &ctl,
-                                              const StepShared &sh, float *cloud, float acc[18],
-                                              float c[8]) {
+                                              const StepShared &sh, float *cloud,
+                                              float acc[18], float c[8]) {
+  constexpr bool TAB = !PERSIST;   // persist blocks spend their shared memory on the clouds
   const int M = P.M;
   const bool has0 = li < M;
   float x[8], zc[7], zn[7];
-  particle_noise<ZARR, NK>(P, t, k, kg, li, zc);
-  if (li + G < M) particle_noise<ZARR, NK>(P, t, k, kg, li + G, zn);
+  // Philox rounds 0-2 minus the particle index: once per (k, t)
+  const BeliefPrefix bp = ZARR ? BeliefPrefix{} : belief_prefix(P.kb, (uint32_t)t, (uint32_t)kg);
+  particle_noise<ZARR, NK, TAB>(P, bp, t, k, li, zc);
+  if (li + G < M) particle_noise<ZARR, NK, TAB>(P, bp, t, k, li + G, zn);
   if (has0) particle_step<PERSIST, ZARR, NK, ST>(P, t, li, mean, L, ctl, sh, cloud, zc, x);
 #pragma unroll
   for (int i = 0; i < 8; ++i) c[i] = __shfl_sync(0xffffffffu, x[i], 0, G);
-  if (has0) accumulate<!PERSIST>(acc, x, c);
+  // persist clouds need the wheel sums too (scalar form); re-projected
+  // particles use the packed sums
+  AccPacked A{};
+  const float2 nc[3] = {make_float2(-c[0], -c[7]), make_float2(-c[1], -c[2]), make_float2(-c[5], -c[6])};
+  const auto add = [&](const float x_[8]) {
+    if (PERSIST) accumulate<false>(acc, x_, c);
+    else accumulate_packed(A, x_, nc);
+  };
+  if (has0) add(x);
   int m = li + G;
   // unrolled twice: the look-ahead noise alternates between two register
   // sets instead of being copied (7 moves) at every particle
@@ -478,14 +541,15 @@ __device__ __forceinline__ void particle_pass(const RollParams &P, int t, int k,
   for (; m + G < M; m += G) {             // steady state: look one particle ahead
 #pragma unroll
     for (int j = 0; j < 7; ++j) zc[j] = zn[j];
-    particle_noise<ZARR, NK>(P, t, k, kg, m + G, zn);
+    particle_noise<ZARR, NK, TAB>(P, bp, t, k, m + G, zn);
     particle_step<PERSIST, ZARR, NK, ST>(P, t, m, mean, L, ctl, sh, cloud, zc, x);
-    accumulate<!PERSIST>(acc, x, c);
+    add(x);
   }
   if (m < M) {                            // last particle: no look-ahead draw
     particle_step<PERSIST, ZARR, NK, ST>(P, t, m, mean, L, ctl, sh, cloud, zn, x);
-    accumulate<!PERSIST>(acc, x, c);
+    add(x);
   }
+  if (!PERSIST) unpack_acc(A, acc);
 }
 
 // BSS rollouts.  G: lanes per rollout; PERSIST: keep the particle cloud in
@@ -606,8 +670,14 @@ __device__ __forceinline__ void bss_rollout(const RollParams &P) {
       sh = step_shared(mean, CtlDev{cv.x, cv.y, cv.z, cv.w}, P.V, P.tr, kap_mean);
     }
   }
-  total += P.term * stage_cost(mean, P) + shield_penalty(h_cur, h_prev, P);
-  if (P.n_obs) total += P.term * (inside ? P.c_obs : 0.f) + shield_penalty(ho_cur, ho_prev, P);
+  // two separate adds, in the reference's order (controllers.py:318-319):
+  // the det kernel adds them the same way, so BSS == S-MPPI stays bit-exact
+  total += __fmul_rn(P.term, stage_cost(mean, P));
+  total += shield_penalty(h_cur, h_prev, P);
+  if (P.n_obs) {
+    total += __fmul_rn(P.term, inside ? P.c_obs : 0.f);
+    total += shield_penalty(ho_cur, ho_prev, P);
+  }
   if (active && li == 0) P.cost_out[k] = dead ? __int_as_float(0x7f800000) : total;
 }
 
@@ -620,17 +690,31 @@ __device__ __forceinline__ void bss_rollout(const RollParams &P) {
 // range: every variant's T loop holds exactly one particle loop.
 template <int G, bool PERSIST, bool ZARR, bool ST, int BT>
 __device__ __forceinline__ void bss_rollout_nk(const RollParams &P) {
+#ifdef BSS_AB_ONLY   // quick A/B builds (tools/build_variants.sh): the hot variant only
+  bss_rollout<G, PERSIST, ZARR, NK_GAUSS_DIAG, ST, BT>(P);
+#else
   if (!ZARR && P.noise_kind == 1) bss_rollout<G, PERSIST, ZARR, NK_LAPLACE, ST, BT>(P);
   else if (P.noise_diag) bss_rollout<G, PERSIST, ZARR, NK_GAUSS_DIAG, ST, BT>(P);
   else bss_rollout<G, PERSIST, ZARR, NK_GAUSS_GENERAL, ST, BT>(P);
+#endif
 }
 
 // BT: block threads, a compile-time constant (128, or 512 for the one-wave
 // shapes of bssmppi.cu rollout_block_threads); same register budget.
 template <int G, bool PERSIST, bool ZARR, int BT = kBlockThreads>
 __global__ void BSS_ROLLOUT_BOUNDS bss_rollout_kernel(const RollParams P) {
+  // Box-Muller angle table (philox.cuh angle_entry), built once per block:
+  // the kernel's one block-wide barrier, before any warp can retire
+  if (!PERSIST && !ZARR) {
+    for (int j = threadIdx.x; j < kAngleTab; j += BT) g_angle_tab[j] = angle_entry((uint32_t)j);
+    __syncthreads();
+  }
+#ifdef BSS_AB_ONLY
+  bss_rollout_nk<G, PERSIST, ZARR, true, BT>(P);
+#else
   if (P.V.tire_short) bss_rollout_nk<G, PERSIST, ZARR, true, BT>(P);
   else bss_rollout_nk<G, PERSIST, ZARR, false, BT>(P);
+#endif
 }
 
 // Deterministic rollouts for kind "mppi" / "smppi" (controllers.py:320-338):
@@ -670,10 +754,10 @@ __device__ __forceinline__ void det_rollout(const RollParams &P) {
       ho_cur = obstacle_terms(P, x[7], x[6], 0.f, inside);
     }
   }
-  total += P.term * stage_cost(x, P);
+  total += __fmul_rn(P.term, stage_cost(x, P));
   if (SHIELD) total += shield_penalty(h_cur, h_prev, P);
   if (P.n_obs) {
-    total += P.term * (inside ? P.c_obs : 0.f);
+    total += __fmul_rn(P.term, inside ? P.c_obs : 0.f);
     if (SHIELD) total += shield_penalty(ho_cur, ho_prev, P);
   }
   P.cost_out[k] = dead ? __int_as_float(0x7f800000) : total;

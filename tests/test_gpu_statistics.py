@@ -76,7 +76,9 @@ def test_mean_cost_per_rollout(draws):
     n = keep.sum()
     print(f"per-rollout mean cost: {n} rollouts, |z| < 3: {np.mean(np.abs(z) < 3):.4f}, "
           f"max |z| {np.abs(z).max():.2f}, mean z {z.mean():+.3f}")
-    assert n > K // 2
+    # power: >= 64 on-track rollouts x R draws (random controls around a
+    # fixed nominal leave about half of K on the track)
+    assert n >= K // 4
     assert np.mean(np.abs(z) < 3.0) >= 0.97          # 0.9973 expected
     assert np.abs(z).max() < 5.0
     assert abs(z.mean()) < 4.0 / math.sqrt(n)          # no common bias
