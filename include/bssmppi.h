@@ -220,6 +220,15 @@ int bssmppi_philox4x32(const uint32_t ctr[4], const uint32_t key[2], int32_t rou
 int bssmppi_belief_normals(const uint32_t key[2], int32_t t, int32_t k, int32_t m_count,
                            float *out /* m_count*7 */);
 
+/* The lateral tire table the kernels evaluate sin(C atan(B alpha)) from
+ * (host-side, no device work; the context builds the same table):
+ * bc = {B_front, C_front, B_rear, C_rear}, steer_max = max |steering bound|.
+ * Writes 2 * rows float4 rows {c0, c1, c2, c3} (front, then rear) into out
+ * (capacity cap rows), rows per axle, cells per radian and the domain end.
+ * Returns BSSMPPI_ERR_INVALID if cap is too small. */
+int bssmppi_tire_table(const double bc[4], double steer_max, float *out, int32_t cap,
+                       int32_t *rows, double *cells_per_rad, double *amax);
+
 /* Per-iteration device-noise key: Philox4x32-10 of (iteration, domain) under
  * the controller's base key (host-side, no device work). */
 int bssmppi_iteration_key(const uint32_t base[2], uint32_t domain, uint64_t iteration,

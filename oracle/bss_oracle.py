@@ -104,14 +104,23 @@ def derivs(x, u0, u1, p, track):
     return dx, ok
 
 
-def step_euler(x, u, p, track, dt):
+def step_euler(x, u, p, track, dt, wrap_when_needed=False):
     """Euler branch of ``_step_kernel`` (dynamics.py:447-497): x + dt f(x),
-    e_psi wrapped to (-pi, pi], s floor-mod L, non-finite -> 0 and ok=False."""
-    u = np.asarray(u, dtype=float)
+    e_psi wrapped to (-pi, pi], s floor-mod L, non-finite -> 0 and ok=False.
+    ``wrap_when_needed`` applies the heading formula only outside (-pi, pi]
+    (where it is the identity in exact arithmetic): the FP32 emulations use
+    it, since the literal formula quantises e_psi to ulp(pi) in FP32."""
+    u = np.asarray(u, dtype=x.dtype)
     with np.errstate(all="ignore"):
         dx, ok = derivs(x, u[..., 0], u[..., 1], p, track)
         out = x + dt * dx
-        out[..., 5] = math.pi - np.mod(math.pi - out[..., 5], 2.0 * math.pi)
+        pi = out.dtype.type(math.pi)
+        wrapped = pi - np.mod(pi - out[..., 5], 2 * pi)
+        if wrap_when_needed:
+            inside = (out[..., 5] > -pi) & (out[..., 5] <= pi)
+            out[..., 5] = np.where(inside, out[..., 5], wrapped)
+        else:
+            out[..., 5] = wrapped
         if track.closed:
             out[..., 7] = np.mod(out[..., 7], track.length)
         else:
@@ -256,7 +265,8 @@ class Problem:
 
 
 def rollout_bss(prob: Problem, x0, cov0, u, eps, nominal, z_all, precision=None,
-                gamma=0.0, persist=False, record=None, dtype=np.float64, round_state=None):
+                gamma=0.0, persist=False, record=None, dtype=np.float64, round_state=None,
+                step_dtype=None, careful=False):
     """Belief rollout costs (``_rollout`` bss branch, controllers.py:261-319, 340).
 
     u: (K, T, 2) clamped controls, eps: (K, T, 2) raw perturbations,
@@ -267,7 +277,14 @@ def rollout_bss(prob: Problem, x0, cov0, u, eps, nominal, z_all, precision=None,
     separates FP32's own conditioning from device deviations.
     ``round_state=np.float32`` keeps FP64 arithmetic but rounds every
     particle state to FP32 after the re-projection and after the step: the
-    irreducible error of holding particles in FP32 registers."""
+    irreducible error of holding particles in FP32 registers.
+    ``step_dtype=np.float32`` (with ``round_state``) additionally evaluates
+    the Euler step -- tire model, derivatives, update -- in FP32 arithmetic
+    (numpy float32 libm, heading wrap only when needed), everything else in
+    FP64: the floor of a careful FP32 implementation of the step.
+    ``careful=True`` with ``dtype=np.float32``: the whole algorithm in FP32
+    except the literal heading-wrap formula (applied only outside (-pi, pi],
+    where it is not the identity) -- a careful FP32 port."""
     rnd = (lambda a: a) if round_state is None else (lambda a: a.astype(round_state).astype(a.dtype))
     K, T, _ = u.shape
     M = z_all.shape[2]
@@ -302,7 +319,15 @@ def rollout_bss(prob: Problem, x0, cov0, u, eps, nominal, z_all, precision=None,
             x[:, :, SUBSET] += np.einsum("kab,kmb->kma", L, z_all[t][:, :, :4])
         x = rnd(x)
         ub = np.repeat(u[:, t][:, None, :], M, axis=1)
-        x1, _ = step_euler(x, ub, prob.p, prob.track, prob.dt)   # per-particle ok discarded
+        if dtype is not np.float64:                      # FP32 port: heading wrap only when needed
+            x1, _ = step_euler(x, ub, prob.p, prob.track, prob.dt, wrap_when_needed=careful)
+        elif step_dtype is not None:
+            p32 = prob.astype(step_dtype)
+            x1, _ = step_euler(x.astype(step_dtype), ub.astype(step_dtype), p32.p, p32.track, p32.dt,
+                               wrap_when_needed=True)
+            x1 = x1.astype(x.dtype)
+        else:
+            x1, _ = step_euler(x, ub, prob.p, prob.track, prob.dt)   # per-particle ok discarded
         if noise_on:                                      # dynamics.py:571-572
             x1[..., 0:3] += z_all[t][:, :, 4:7] @ prob.F.T
         x1 = rnd(x1)

@@ -102,6 +102,7 @@ SIGNATURES = {
     "bssmppi_mufu_peak": (C.c_int, [C.c_int32, _dp]),
     "bssmppi_enqueue_step_device": (C.c_int, [_ctx, C.c_void_p, _u32p, _u32p, C.c_void_p]),
     "bssmppi_iteration_key": (C.c_int, [_u32p, C.c_uint32, C.c_uint64, _u32p]),
+    "bssmppi_tire_table": (C.c_int, [_dp, C.c_double, _fp, C.c_int32, C.POINTER(C.c_int32), _dp, _dp]),
 }
 
 _LIB = None

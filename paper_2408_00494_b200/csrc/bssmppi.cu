@@ -13,6 +13,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <cstdlib>
 #include <string>
 #include <vector>
@@ -66,6 +67,7 @@ struct bssmppi_ctx {
   float *d_u = nullptr, *d_cost = nullptr;
   float4 *d_ctl = nullptr;    // per-(k,t) control table
   float4 *d_obs = nullptr, *d_cl = nullptr;   // config-4 extension tables
+  float4 *d_tire = nullptr;   // lateral tire table (vehicle.cuh tire_q)
   float *d_cc = nullptr;      // per-(k,t) control-cost terms
   double *d_eps = nullptr, *d_uin = nullptr;
   float *d_z = nullptr, *d_mom = nullptr;
@@ -107,9 +109,12 @@ int validate(const bssmppi_problem *p) {
   if (p->kind < 0 || p->kind > 2) return fail(BSSMPPI_ERR_INVALID, "unknown controller kind %d", p->kind);
   if (p->samples < 1 || p->horizon < 1) return fail(BSSMPPI_ERR_INVALID, "samples and horizon must be >= 1");
   if (p->horizon > 512) return fail(BSSMPPI_ERR_UNSUPPORTED, "horizon %d > 512", p->horizon);
-  if (!(p->phys[7] > 0.0 && p->phys[7] <= 2.0 && p->phys[9] > 0.0 && p->phys[9] <= 2.0))
-    return fail(BSSMPPI_ERR_UNSUPPORTED, "lateral magic-formula shape factors C must lie in (0, 2] "
-                "(got %g, %g): the device tire sine covers |C atan(.)| <= pi", p->phys[7], p->phys[9]);
+  if (!(std::isfinite(p->phys[6]) && std::isfinite(p->phys[7]) && std::isfinite(p->phys[8]) &&
+        std::isfinite(p->phys[9])))
+    return fail(BSSMPPI_ERR_INVALID, "lateral magic-formula coefficients must be finite");
+  if (!(std::fabs(p->bounds_lo[0]) <= 2 * M_PI && std::fabs(p->bounds_hi[0]) <= 2 * M_PI))
+    return fail(BSSMPPI_ERR_UNSUPPORTED, "steering bounds beyond +-2 pi (the tire table covers "
+                "|slip angle| <= pi + max |steering bound|)");
   if (!(p->temperature > 0.0)) return fail(BSSMPPI_ERR_INVALID, "temperature must be > 0");
   if (p->kind == BSSMPPI_KIND_BSS && p->inner_samples < 2)
     return fail(BSSMPPI_ERR_INVALID, "bss controller needs inner_samples >= 2");
@@ -160,6 +165,75 @@ int build_extensions(bssmppi_ctx *c, const bssmppi_problem *p) {
   r.cl = c->d_cl;
   r.cl_n = p->centerline_n;
   r.cl_inv_ds = (float)(1.0 / p->centerline_ds);
+  return BSSMPPI_OK;
+}
+
+// Lateral tire table (vehicle.cuh tire_q / lateral_shape): sin(C atan(B a))
+// = a q(|a|) with q(a) = sin(C atan(B a)) / a (even, smooth, q(0) = C B).
+// Rows are centred on a = j / s; each holds the cubic in f = a s - j that
+// interpolates q in FP64 at the four Chebyshev nodes of f in [-1/2, 1/2]
+// (near-minimax).  The domain covers every slip angle a rollout can meet,
+// |alpha| <= pi + max |steering bound|, and the cell width keeps B h <=
+// 0.055: the FP32 evaluation then stays at ~1.9e-7 relative (rounding level)
+// for all B, C (tests/test_tire_table.py).
+constexpr double kTireBh = 0.055;
+constexpr int kTireMaxCells = 2000;   // row index must fit 0x7ff (vehicle.cuh tire_q)
+
+double tire_q_exact(double B, double C, double a) {
+  return std::fabs(a) < 1e-300 ? C * B : std::sin(C * std::atan(B * a)) / a;
+}
+
+void tire_table_host(const double bc[4], double steer_max, std::vector<float4> &tab, double &sc,
+                     double &amax, int &rows) {
+  amax = M_PI + steer_max + 0.01;
+  const double bmax = std::max(bc[0], bc[2]);
+  const int cells = (int)std::min<double>(kTireMaxCells, std::max(64.0, std::ceil(amax * bmax / kTireBh)));
+  sc = cells / amax;
+  rows = cells + 2;
+  tab.assign(2 * (size_t)rows, make_float4(0.f, 0.f, 0.f, 0.f));
+  double nodes[4];
+  for (int i = 0; i < 4; ++i) nodes[i] = -0.5 + 0.5 * (1.0 - std::cos((2 * i + 1) * M_PI / 8.0));
+  for (int axle = 0; axle < 2; ++axle) {
+    const double B = bc[2 * axle], C = bc[2 * axle + 1];
+    for (int j = 0; j < rows; ++j) {
+      double A[4][5];   // Vandermonde system of the interpolating cubic in f
+      for (int i = 0; i < 4; ++i) {
+        double pw = 1.0;
+        for (int k = 0; k < 4; ++k) { A[i][k] = pw; pw *= nodes[i]; }
+        A[i][4] = tire_q_exact(B, C, (j + nodes[i]) / sc);
+      }
+      for (int k = 0; k < 4; ++k) {            // Gauss-Jordan, partial pivoting
+        int piv = k;
+        for (int i = k + 1; i < 4; ++i) if (std::fabs(A[i][k]) > std::fabs(A[piv][k])) piv = i;
+        for (int m = 0; m < 5; ++m) std::swap(A[k][m], A[piv][m]);
+        for (int i = 0; i < 4; ++i) {
+          if (i == k) continue;
+          const double f = A[i][k] / A[k][k];
+          for (int m = k; m < 5; ++m) A[i][m] -= f * A[k][m];
+        }
+      }
+      tab[(size_t)axle * rows + j] = make_float4((float)(A[0][4] / A[0][0]), (float)(A[1][4] / A[1][1]),
+                                                 (float)(A[2][4] / A[2][2]), (float)(A[3][4] / A[3][3]));
+    }
+  }
+}
+
+int build_tire_table(bssmppi_ctx *c, const bssmppi_problem *p) {
+  const double *q = p->phys;
+  const double bc[4] = {q[6], q[7], q[8], q[9]};
+  std::vector<float4> tab;
+  double sc, amax;
+  int rows;
+  tire_table_host(bc, std::max(std::fabs(p->bounds_lo[0]), std::fabs(p->bounds_hi[0])), tab, sc, amax, rows);
+  int rc;
+  if ((rc = dev_alloc(&c->d_tire, tab.size()))) return rc;
+  CUDA_TRY(cudaMemcpy(c->d_tire, tab.data(), tab.size() * sizeof(float4), cudaMemcpyHostToDevice));
+  VehDev &Vd = c->rp.V;
+  Vd.tire = c->d_tire;
+  Vd.tire_s = (float)sc;
+  Vd.tire_amax = (float)amax;
+  Vd.tire_rows = rows;
+  Vd.tire_smem = rows <= kTireSmemRows ? 1 : 0;
   return BSSMPPI_OK;
 }
 
@@ -231,7 +305,6 @@ void fill_params(bssmppi_ctx *c, const bssmppi_problem *p) {
   V.dt_lf_iz = (float)(p->dt * q[2] / q[1]);
   V.ndt_lr_iz = (float)(-p->dt * q[3] / q[1]);
   V.dt_m = (float)(p->dt / q[0]);
-  V.tire_short = std::max(q[7], q[9]) * (M_PI / 2.0) <= 2.2 ? 1 : 0;
   V.Cy = make_float2(V.Cyf, V.Cyr);
   V.Dy = make_float2(V.Dyf, V.Dyr);
   V.Bx = make_float2(V.Bxf, V.Bxr);
@@ -327,6 +400,22 @@ int rollout_block_threads(int k_count, int G, bool persist, bool zarr, int sms) 
   return (warps >= (long long)(BSS_BIG_MIN_FRAC * wave) && warps <= wave) ? kMaxBlockThreads : kBlockThreads;
 }
 
+// Static shared memory of a kernel (cached: cudaFuncGetAttributes is a
+// driver query, and launches sit on the host latency path of small K).
+size_t static_smem_of(const void *fn) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void *, size_t>> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  for (const auto &e : cache)
+    if (e.first == fn) return e.second;
+  cudaFuncAttributes a{};
+  const size_t v = cudaFuncGetAttributes(&a, fn) == cudaSuccess ? a.sharedSizeBytes : 48 * 1024;
+  cache.emplace_back(fn, v);
+  return v;
+}
+template <typename F>
+size_t static_smem_of(F *fn) { return static_smem_of(reinterpret_cast<const void *>(fn)); }
+
 template <int G>
 cudaError_t launch_bss_g(const RollParams &rp, bool persist, bool zarr, int sms, cudaStream_t st) {
   const int threads = rollout_block_threads(rp.k_count, G, persist, zarr, sms);
@@ -349,10 +438,10 @@ cudaError_t launch_bss_g(const RollParams &rp, bool persist, bool zarr, int sms,
   }
   else fn = bss_rollout_kernel<G, false, false>;
 #endif
-  // the Philox kernels also hold the 32 KB Box-Muller angle table (static):
-  // past 48 KB in total the dynamic part needs the opt-in attribute
-  const size_t static_smem = (persist || zarr) ? 0 : (size_t)kAngleTab * sizeof(float2);
-  if (smem + static_smem > 48 * 1024) {
+  // the kernels also hold static tables (Box-Muller angles, the tire
+  // table's shared copy): past 48 KB in total the dynamic part needs the
+  // opt-in attribute
+  if (smem + static_smem_of(fn) > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
@@ -561,6 +650,7 @@ int bssmppi_create(const bssmppi_problem *problem, int32_t device, bssmppi_ctx *
   auto bail = [&](int code) { bssmppi_destroy(c); return code; };
   if ((rc = build_track(c, problem))) return bail(rc);
   if ((rc = build_extensions(c, problem))) return bail(rc);
+  if ((rc = build_tire_table(c, problem))) return bail(rc);
   const int T2 = 2 * c->T;
   c->nblocks = std::min(1024, std::max(1, std::min((c->k_count + 63) / 64, 2 * 148)));
   c->chunk = (c->k_count + c->nblocks - 1) / c->nblocks;
@@ -590,7 +680,7 @@ void bssmppi_destroy(bssmppi_ctx *c) {
   DeviceGuard guard(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   cudaFree(c->d_node); cudaFree(c->d_cell); cudaFree(c->d_state); cudaFree(c->d_u);
-  cudaFree(c->d_cost); cudaFree(c->d_ctl); cudaFree(c->d_cc); cudaFree(c->d_obs); cudaFree(c->d_cl); cudaFree(c->d_eps); cudaFree(c->d_uin); cudaFree(c->d_z);
+  cudaFree(c->d_cost); cudaFree(c->d_ctl); cudaFree(c->d_cc); cudaFree(c->d_obs); cudaFree(c->d_cl); cudaFree(c->d_tire); cudaFree(c->d_eps); cudaFree(c->d_uin); cudaFree(c->d_z);
   cudaFree(c->d_mom); cudaFree(c->d_rec); cudaFree(c->d_out);
   if (c->h_state) cudaFreeHost(c->h_state);
   if (c->h_out) cudaFreeHost(c->h_out);
@@ -991,6 +1081,19 @@ int bssmppi_mufu_peak(int32_t device, double *tops) {
   if (e != cudaSuccess) return fail(BSSMPPI_ERR_CUDA, "mufu_peak: %s", cudaGetErrorString(e));
   const double ops = 8.0 * 16 * (double)iters * blocks * 256;
   *tops = ops / (ms * 1e-3) / 1e12;
+  return BSSMPPI_OK;
+}
+
+int bssmppi_tire_table(const double bc[4], double steer_max, float *out, int32_t cap, int32_t *rows,
+                       double *cells_per_rad, double *amax) {
+  if (!bc || !out || !rows || !cells_per_rad || !amax || !(steer_max >= 0.0))
+    return fail(BSSMPPI_ERR_INVALID, "bad tire_table arguments");
+  std::vector<float4> tab;
+  int r;
+  tire_table_host(bc, steer_max, tab, *cells_per_rad, *amax, r);
+  *rows = r;
+  if ((size_t)cap < tab.size()) return fail(BSSMPPI_ERR_INVALID, "tire_table needs %zu rows", tab.size());
+  std::memcpy(out, tab.data(), tab.size() * sizeof(float4));
   return BSSMPPI_OK;
 }
 

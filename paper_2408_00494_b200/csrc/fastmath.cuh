@@ -93,38 +93,6 @@ __device__ __forceinline__ float2 atan2_x2(float2 x, float2 Y, float2 rev) {
   return make_float2(copysignf(m.x, Y.x), copysignf(m.y, Y.y));
 }
 
-// sin of two arguments in [-pi, pi] (the sincos_pi sine polynomial, packed;
-// ~1 ulp, relative accuracy kept near 0 unlike MUFU.SIN's absolute 2^-21.4).
-__device__ __forceinline__ float2 sin_pi_x2(float2 x) {
-  const float2 t = __fmul2_rn(x, x);
-  float2 p = __ffma2_rn(t, bc2(-6.416872784e-13f), bc2(1.582333015e-10f));
-  p = __ffma2_rn(p, t, bc2(-2.502759777e-08f));
-  p = __ffma2_rn(p, t, bc2(2.755584774e-06f));
-  p = __ffma2_rn(p, t, bc2(-1.984121918e-04f));
-  p = __ffma2_rn(p, t, bc2(8.333332837e-03f));
-  p = __ffma2_rn(p, t, bc2(-1.666666716e-01f));
-  p = __ffma2_rn(p, t, bc2(1.0f));
-  return __fmul2_rn(p, x);
-}
-
-// sin of two magic-formula arguments, |x| <= 2.2 (lateral shape factors
-// C <= 1.40, incl. the reference default 1.3): sin x = x (1 + t Q(t)),
-// t = x^2, Q of degree 4 fitted with the constant term held at exactly 1
-// (tools/fit_poly.py sin_tire: 2.1e-7 absolute / 2.6e-7 relative on the
-// range, the sin_pi_x2 level) -- two FFMA2 (four FMA-pipe cycles) fewer.
-// SHORT = false is sin_pi_x2 (|x| <= pi, C <= 2).
-template <bool SHORT>
-__device__ __forceinline__ float2 sin_tire_x2(float2 x) {
-  if (!SHORT) return sin_pi_x2(x);
-  const float2 t = __fmul2_rn(x, x);
-  float2 p = __ffma2_rn(t, bc2(-2.277197275e-08f), bc2(2.743227014e-06f));
-  p = __ffma2_rn(p, t, bc2(-1.983809780e-04f));
-  p = __ffma2_rn(p, t, bc2(8.333297446e-03f));
-  p = __ffma2_rn(p, t, bc2(-1.666666567e-01f));
-  p = __ffma2_rn(p, t, bc2(1.0f));
-  return __fmul2_rn(p, x);
-}
-
 // (sin, cos) on [0, pi/2] in one packed Horner chain: lane x the sine
 // x S(t) (degree 4 in t = x^2, padded with a leading 0), lane y the cosine
 // C(t) (degree 5); tools/fit_poly.py sincos_half: 1.2e-7 / 1.0e-7 absolute,

@@ -344,9 +344,12 @@ __device__ __forceinline__ float control_prologue(const RollParams &P, int k, in
     control_at(P, k, kg, t, u0, u1, c);
     if (active) {
       reinterpret_cast<float2 *>(P.u_out)[row + t] = make_float2(u0, u1);
+      // the steering the dynamics see stays inside the bounds the tire
+      // table is sized for (a no-op except for out-of-bounds given controls)
+      const float dl = fminf(fmaxf(u0, P.lo[0]), P.hi[0]);
       float sd, cd;
-      sincosf(u0, &sd, &cd);
-      P.ctl[row + t] = make_float4(u0, cd, sd, P.V.drive * u1);
+      sincosf(dl, &sd, &cd);
+      P.ctl[row + t] = make_float4(dl, cd, sd, P.V.drive * u1);
       P.ccost[row + t] = c;
     }
   }
@@ -395,7 +398,7 @@ __device__ __forceinline__ void particle_noise(const RollParams &P, const Belief
 
 // One particle-step given its noise: re-project (or load the persistent
 // particle), Euler step, process noise.  Returns the post-step state in x.
-template <bool PERSIST, bool ZARR, int NK, bool ST>
+template <bool PERSIST, bool ZARR, int NK, bool TS>
 __device__ __forceinline__ void particle_step(const RollParams &P, int t, int m, const float mean[8],
                                               const float L[10], const CtlDev &ctl, const StepShared &sh,
                                               float *cloud, const float z[7], float x[8]) {
@@ -422,8 +425,8 @@ __device__ __forceinline__ void particle_step(const RollParams &P, int t, int m,
   }
   // per-particle ok is discarded (belief.py:370); a re-projected particle
   // shares (vx, omega_f, omega_r, s) with the mean, hence the shared terms
-  if (PERSIST && t > 0) vehicle_step<ST>(x, ctl, P.V, P.tr);
-  else step_particle<ST>(x, sh, ctl, P.V, P.tr);
+  if (PERSIST && t > 0) vehicle_step<TS>(x, ctl, P.V, P.tr);
+  else step_particle<TS>(x, sh, ctl, P.V, P.tr);
   if (NK == NK_LAPLACE) {                // config-4 extension, after integration too
     x[0] += z[4];
     x[1] += z[5];
@@ -509,7 +512,7 @@ __device__ __forceinline__ void unpack_acc(const AccPacked &A, float acc[18]) {
 // particle m + G are produced inside particle m's iteration, so the
 // quarter-rate IMAD.WIDE / MUFU work overlaps the FP32 dynamics in one
 // scheduling region; the last particle is peeled, so no draw is wasted.
-template <int G, bool PERSIST, bool ZARR, int NK, bool ST>
+template <int G, bool PERSIST, bool ZARR, int NK, bool TS>
 __device__ __forceinline__ void particle_pass(const RollParams &P, int t, int k, int kg, int li,
                                               const float mean[8], const float L[10], const CtlDev &ctl,
                                               const StepShared &sh, float *cloud,
@@ -522,7 +525,7 @@ __device__ __forceinline__ void particle_pass(const RollParams &P, int t, int k,
   const BeliefPrefix bp = ZARR ? BeliefPrefix{} : belief_prefix(P.kb, (uint32_t)t, (uint32_t)kg);
   particle_noise<ZARR, NK, TAB>(P, bp, t, k, li, zc);
   if (li + G < M) particle_noise<ZARR, NK, TAB>(P, bp, t, k, li + G, zn);
-  if (has0) particle_step<PERSIST, ZARR, NK, ST>(P, t, li, mean, L, ctl, sh, cloud, zc, x);
+  if (has0) particle_step<PERSIST, ZARR, NK, TS>(P, t, li, mean, L, ctl, sh, cloud, zc, x);
 #pragma unroll
   for (int i = 0; i < 8; ++i) c[i] = __shfl_sync(0xffffffffu, x[i], 0, G);
   // persist clouds need the wheel sums too (scalar form); re-projected
@@ -542,11 +545,11 @@ __device__ __forceinline__ void particle_pass(const RollParams &P, int t, int k,
 #pragma unroll
     for (int j = 0; j < 7; ++j) zc[j] = zn[j];
     particle_noise<ZARR, NK, TAB>(P, bp, t, k, m + G, zn);
-    particle_step<PERSIST, ZARR, NK, ST>(P, t, m, mean, L, ctl, sh, cloud, zc, x);
+    particle_step<PERSIST, ZARR, NK, TS>(P, t, m, mean, L, ctl, sh, cloud, zc, x);
     add(x);
   }
   if (m < M) {                            // last particle: no look-ahead draw
-    particle_step<PERSIST, ZARR, NK, ST>(P, t, m, mean, L, ctl, sh, cloud, zn, x);
+    particle_step<PERSIST, ZARR, NK, TS>(P, t, m, mean, L, ctl, sh, cloud, zn, x);
     add(x);
   }
   if (!PERSIST) unpack_acc(A, acc);
@@ -557,7 +560,7 @@ __device__ __forceinline__ void particle_pass(const RollParams &P, int t, int k,
 // ZARR: read the reference's normals instead of Philox; NK: the process
 // noise kind (NoiseKind), resolved once at kernel entry so every variant's
 // T loop holds exactly one particle loop (register allocation per variant).
-template <int G, bool PERSIST, bool ZARR, int NK, bool ST, int BT>
+template <int G, bool PERSIST, bool ZARR, int NK, bool TS, int BT>
 __device__ __forceinline__ void bss_rollout(const RollParams &P) {
   extern __shared__ float4 smem4[];
   float *smem = reinterpret_cast<float *>(smem4);
@@ -616,7 +619,7 @@ __device__ __forceinline__ void bss_rollout(const RollParams &P) {
 #pragma unroll
     for (int i = 0; i < 18; ++i) acc[i] = 0.f;
     float c[8];
-    particle_pass<G, PERSIST, ZARR, NK, ST>(P, t, k, kg, li, mean, L, ctl, sh, cloud, acc, c);
+    particle_pass<G, PERSIST, ZARR, NK, TS>(P, t, k, kg, li, mean, L, ctl, sh, cloud, acc, c);
     if (t + 1 < P.T) cv = ctl_row[t + 1];
     group_allreduce18<G>(acc, li, slots + (t & 1) * kSlotFloats);
 
@@ -688,14 +691,14 @@ __device__ __forceinline__ void bss_rollout(const RollParams &P) {
 #endif
 // Kernel-entry dispatch on the launch-constant noise kind and tire-sine
 // range: every variant's T loop holds exactly one particle loop.
-template <int G, bool PERSIST, bool ZARR, bool ST, int BT>
+template <int G, bool PERSIST, bool ZARR, bool TS, int BT>
 __device__ __forceinline__ void bss_rollout_nk(const RollParams &P) {
 #ifdef BSS_AB_ONLY   // quick A/B builds (tools/build_variants.sh): the hot variant only
-  bss_rollout<G, PERSIST, ZARR, NK_GAUSS_DIAG, ST, BT>(P);
+  bss_rollout<G, PERSIST, ZARR, NK_GAUSS_DIAG, TS, BT>(P);
 #else
-  if (!ZARR && P.noise_kind == 1) bss_rollout<G, PERSIST, ZARR, NK_LAPLACE, ST, BT>(P);
-  else if (P.noise_diag) bss_rollout<G, PERSIST, ZARR, NK_GAUSS_DIAG, ST, BT>(P);
-  else bss_rollout<G, PERSIST, ZARR, NK_GAUSS_GENERAL, ST, BT>(P);
+  if (!ZARR && P.noise_kind == 1) bss_rollout<G, PERSIST, ZARR, NK_LAPLACE, TS, BT>(P);
+  else if (P.noise_diag) bss_rollout<G, PERSIST, ZARR, NK_GAUSS_DIAG, TS, BT>(P);
+  else bss_rollout<G, PERSIST, ZARR, NK_GAUSS_GENERAL, TS, BT>(P);
 #endif
 }
 
@@ -703,23 +706,34 @@ __device__ __forceinline__ void bss_rollout_nk(const RollParams &P) {
 // shapes of bssmppi.cu rollout_block_threads); same register budget.
 template <int G, bool PERSIST, bool ZARR, int BT = kBlockThreads>
 __global__ void BSS_ROLLOUT_BOUNDS bss_rollout_kernel(const RollParams P) {
-  // Box-Muller angle table (philox.cuh angle_entry), built once per block:
-  // the kernel's one block-wide barrier, before any warp can retire
-  if (!PERSIST && !ZARR) {
+  // Shared tables, built once per block -- the Box-Muller angle table
+  // (philox.cuh angle_entry) and a copy of the tire table (vehicle.cuh;
+  // persist blocks keep their shared memory for the clouds) -- then the
+  // kernel's one block-wide barrier, before any warp can retire.
+  const bool ts = !PERSIST && P.V.tire_smem;
+  if (!PERSIST && !ZARR)
     for (int j = threadIdx.x; j < kAngleTab; j += BT) g_angle_tab[j] = angle_entry((uint32_t)j);
-    __syncthreads();
-  }
+  if (ts)
+    for (int j = threadIdx.x; j < 2 * P.V.tire_rows; j += BT) {
+      const int axle = j >= P.V.tire_rows, row = j - axle * P.V.tire_rows;
+      g_tire_tab[axle * kTireSmemRows + row] = __ldg(P.V.tire + j);
+    }
+  if (!PERSIST) __syncthreads();
 #ifdef BSS_AB_ONLY
   bss_rollout_nk<G, PERSIST, ZARR, true, BT>(P);
 #else
-  if (P.V.tire_short) bss_rollout_nk<G, PERSIST, ZARR, true, BT>(P);
-  else bss_rollout_nk<G, PERSIST, ZARR, false, BT>(P);
+  if constexpr (PERSIST) {
+    bss_rollout_nk<G, PERSIST, ZARR, false, BT>(P);
+  } else {
+    if (ts) bss_rollout_nk<G, PERSIST, ZARR, true, BT>(P);
+    else bss_rollout_nk<G, PERSIST, ZARR, false, BT>(P);
+  }
 #endif
 }
 
 // Deterministic rollouts for kind "mppi" / "smppi" (controllers.py:320-338):
 // one lane per k, state carried in registers.
-template <bool SHIELD, bool ST>
+template <bool SHIELD>
 __device__ __forceinline__ void det_rollout(const RollParams &P) {
   const int kraw = blockIdx.x * kBlockThreads + threadIdx.x;
   if (kraw >= P.k_count) return;
@@ -743,7 +757,7 @@ __device__ __forceinline__ void det_rollout(const RollParams &P) {
       if (SHIELD && t > 0) total += shield_penalty(ho_cur, ho_prev, P);
     }
     const float4 cv = ctl_row[t];
-    const bool ok = vehicle_step<ST>(x, CtlDev{cv.x, cv.y, cv.z, cv.w}, P.V, P.tr);
+    const bool ok = vehicle_step<false>(x, CtlDev{cv.x, cv.y, cv.z, cv.w}, P.V, P.tr);
     dead |= !ok;
     if (SHIELD) {
       h_prev = h_cur;
@@ -765,12 +779,10 @@ __device__ __forceinline__ void det_rollout(const RollParams &P) {
 
 template <bool SHIELD>
 __global__ void __launch_bounds__(kBlockThreads) det_rollout_kernel(const RollParams P) {
-  if (P.V.tire_short) det_rollout<SHIELD, true>(P);
-  else det_rollout<SHIELD, false>(P);
+  det_rollout<SHIELD>(P);
 }
 
 // step_array (dynamics.py:550-573): one particle per thread, FP64 I/O.
-template <bool ST>
 __device__ __forceinline__ void step_array(const VehDev &V, const TrackDev &tr, int n, const double *x,
                                            const double *u, const double *w, double *xo, uint8_t *oko) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -778,7 +790,7 @@ __device__ __forceinline__ void step_array(const VehDev &V, const TrackDev &tr, 
   float s[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) s[j] = (float)x[(size_t)i * 8 + j];
-  const bool ok = vehicle_step<ST>(s, make_ctl((float)u[2 * (size_t)i], (float)u[2 * (size_t)i + 1], V), V, tr);
+  const bool ok = vehicle_step<false>(s, make_ctl((float)u[2 * (size_t)i], (float)u[2 * (size_t)i + 1], V), V, tr);
   if (w != nullptr) {
 #pragma unroll
     for (int j = 0; j < 3; ++j) s[j] += (float)w[(size_t)i * 3 + j];
@@ -790,8 +802,7 @@ __device__ __forceinline__ void step_array(const VehDev &V, const TrackDev &tr, 
 
 __global__ void step_array_kernel(VehDev V, TrackDev tr, int n, const double *x, const double *u,
                                   const double *w, double *xo, uint8_t *oko) {
-  if (V.tire_short) step_array<true>(V, tr, n, x, u, w, xo, oko);
-  else step_array<false>(V, tr, n, x, u, w, xo, oko);
+  step_array(V, tr, n, x, u, w, xo, oko);
 }
 
 }  // namespace bss

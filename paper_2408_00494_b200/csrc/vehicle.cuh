@@ -43,8 +43,21 @@ struct VehDev {
   float2 nBy;      // (-Byf, -Byr): the lateral-slip pair as one FFMA2 on (atan2 f, atan2 r)
   float dt_lf_iz, ndt_lr_iz;   // dt lf / Iz, -dt lr / Iz: the yaw-rate Euler update
   float dt_m;                  // dt / m: the (vx, vy) Euler update
-  int tire_short;              // max lateral C pi / 2 <= 2.2: kernels run step_particle<true>
+  // lateral magic formula sin(C atan(B alpha)) = alpha q(|alpha|) as a
+  // piecewise-cubic table of q (build_tire_table in bssmppi.cu): rows
+  // [front | rear] of tire_rows float4 {c0, c1, c2, c3}; row j is centred on
+  // |alpha| = j / tire_s and evaluated at f = |alpha| tire_s - j in [-1/2, 1/2]
+  const float4 *tire;          // device copy (global memory)
+  float tire_s;                // cells per radian
+  float tire_amax;             // table domain [0, tire_amax]: |alpha| beyond it -> libdevice (step kernels)
+  int tire_rows;               // rows per axle (cells + 2)
+  int tire_smem;               // both axles fit g_tire_tab: belief kernels read the shared copy
 };
+
+// Shared copy of the tire table in the belief kernels (rows of the front
+// axle, then the rear's, at stride kTireSmemRows).
+constexpr int kTireSmemRows = 330;
+__shared__ __align__(16) float4 g_tire_tab[2 * kTireSmemRows];
 
 // node[j] = {s_j, kappa_j, slope_j, s_{j+1}} plus a sentinel node[n].
 struct TrackDev {
@@ -289,7 +302,7 @@ __device__ __forceinline__ StepShared step_shared(const float x[8], const CtlDev
 // and finite).
 #ifdef BSS_EXACT_MATH
 // libdevice reference form (A/B parity builds, build_cuda(exact=True)).
-template <bool ST = false>
+template <bool TS = false>
 __device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, const CtlDev &c,
                                               const VehDev &V, const TrackDev &tr) {
   const float vx = x[0], vy = x[1], r = x[2], ep = x[5], ey = x[6], s = x[7];
@@ -327,13 +340,47 @@ __device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, c
 }
 
 #else
+// q(|alpha|) of one axle from its table rows: nearest-row index by the
+// 1.5 2^23 rounding trick (the row number ends up in the low mantissa bits,
+// no F2I), the in-cell offset by one FFMA, the cubic by three.  NaN / inf
+// arguments read row 0 and propagate through f.
+template <bool TS>
+__device__ __forceinline__ float tire_q(float a, const VehDev &V, int axle) {
+  const float MAGIC = 12582912.0f;   // 1.5 2^23
+  if (!TS) {   // step kernels: arbitrary steering; keep the row in range (NaN stays NaN)
+    asm("min.NaN.f32 %0, %0, %1;" : "+f"(a) : "f"(V.tire_amax));
+  }
+  const float nf = fmaf(a, V.tire_s, MAGIC);
+  const float f = fmaf(a, V.tire_s, -(nf - MAGIC));
+  const uint32_t j = __float_as_uint(nf) & 0x7ffu;
+  float4 c;
+  if (TS) c = g_tire_tab[axle * kTireSmemRows + j];
+  else c = __ldg(V.tire + axle * V.tire_rows + j);
+  return fmaf(fmaf(fmaf(c.w, f, c.z), f, c.y), f, c.x);
+}
+
+// (sin(Cf atan(Bf af)), sin(Cr atan(Br ar))) for alpha = (af, ar).  The
+// rollouts' slip angles stay inside the table domain (|atan2| <= pi and the
+// steering is clamped to its bounds, which size the table); the step kernels
+// also take arbitrary steering and fall back to libdevice beyond it.
+template <bool TS>
+__device__ __forceinline__ float2 lateral_shape(float2 al, const VehDev &V) {
+  const float2 q = make_float2(tire_q<TS>(fabsf(al.x), V, 0), tire_q<TS>(fabsf(al.y), V, 1));
+  float2 g = __fmul2_rn(al, q);
+  if (!TS && __builtin_expect(fmaxf(fabsf(al.x), fabsf(al.y)) > V.tire_amax, 0)) {
+    if (fabsf(al.x) > V.tire_amax) g.x = sinf(V.Cyf * atanf(V.Byf * al.x));
+    if (fabsf(al.y) > V.tire_amax) g.y = sinf(V.Cyr * atanf(V.Byr * al.y));
+  }
+  return g;
+}
+
 // Packed form of the same step: the front/rear pairs (slip-angle arguments,
 // both arctangent chains, lateral forces), the heading sin/cos polynomials
 // and the (vx, vy) / (e_psi, e_y) Euler updates run as FP32x2 lanes, one
 // issue slot per pair.  Every lane is an IEEE FMA/MUL/ADD, so all kernels
 // (which share this function) stay bit-identical to one another.
-// ST: short tire sine (sin_tire_x2<true>, lateral C <= 1.40; VehDev::tire_short).
-template <bool ST = false>
+// TS: the tire table is the belief kernel's shared copy (else global memory).
+template <bool TS = false>
 __device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, const CtlDev &c,
                                               const VehDev &V, const TrackDev &tr) {
   const float vx = x[0], vy = x[1], r = x[2], ep = x[5], ey = x[6], s = x[7];
@@ -344,11 +391,9 @@ __device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, c
   // lose it)
   const float2 Y = __ffma2_rn(bc2(r), V.lf_nlr, bc2(vy));
   const float2 A = atan2_x2(__fmul2_rn(Y, bc2(h.rx)), Y, h.rev);
-  // (B_f alpha_f, B_r alpha_r) = (Byf delta - Byf A.x, -Byr A.y): alpha_f =
-  // delta - A.x, alpha_r = -A.y
-  const float2 ty = __fmul2_rn(V.Cy, atan_x2(make_float2(fmaf(V.nBy.x, A.x, h.byd.x), V.nBy.y * A.y)));
-  // |ty| < C pi / 2 <= pi (lateral C <= 2, checked at context creation)
-  const float2 fy = __fmul2_rn(h.dycx, sin_tire_x2<ST>(ty));
+  // slip angles alpha_f = delta - A.x, alpha_r = -A.y; lateral forces
+  // D |cos|_long sin(C atan(B alpha)) from the tire table
+  const float2 fy = __fmul2_rn(h.dycx, lateral_shape<TS>(make_float2(c.delta - A.x, -A.y), V));
   // body-frame front force + rear longitudinal: (fxf cd - fyf sd + fxr, fxf sd + fyf cd)
   const float2 fb = __ffma2_rn(bc2(fy.x), h.nsd_cd, h.fb0);
   float frame = 1.f - h.kap * ey;
@@ -378,11 +423,11 @@ __device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, c
 }
 #endif
 
-template <bool ST = false>
+template <bool TS = false>
 __device__ __forceinline__ bool vehicle_step(float x[8], const CtlDev &c, const VehDev &V,
                                              const TrackDev &tr) {
   const StepShared h = step_shared(x, c, V, tr, curvature(tr, x[7]));
-  return step_particle<ST>(x, h, c, V, tr);
+  return step_particle<TS>(x, h, c, V, tr);
 }
 
 __device__ __forceinline__ CtlDev make_ctl(float delta, float throttle, const VehDev &V) {

@@ -35,6 +35,7 @@ class Inputs:
     def __init__(self, name):
         from oracle import bss_oracle as orc
 
+        self.name = name
         self.meta, self.gold = load_golden(name)
         case = self.case = case_by_name(name)
         (self.cfg, self.cost, self.model, self.track, self.noise, self.x0, self.cov0,
@@ -128,6 +129,15 @@ def moments_rel_err(mean_a, cov_a, mean_b, cov_b, spread=None):
         return 0.0, 0.0
     em, ec = moments_err_arrays(mean_a, cov_a, mean_b, cov_b, spread)
     return float(np.max(em)), float(np.max(ec))
+
+
+def fp32_jitter_floor(name):
+    """Largest belief-mean error of 8 careful FP32 ports of the reference
+    that differ only in +-1 ulp roundings of the mean (committed fixture,
+    tests/golden/make_fp32_floor.py); 0 for cases without an entry."""
+    import json
+    d = json.loads((GOLDEN / "fp32_floor.json").read_text())
+    return d["cases"].get(name, {}).get("mean_max", 0.0)
 
 
 def fp32_state_floor(inp, ks=None):

@@ -71,10 +71,12 @@ def test_validation_before_cuda():
     assert b"samples" in lib.bssmppi_last_error()
 
 
-def test_lateral_shape_factor_range_checked_before_cuda():
-    """The device tire sine covers |C atan(.)| <= pi: a lateral magic-formula
-    shape factor above 2 is refused at context creation (before any CUDA
-    call) instead of returning wrong forces."""
+def test_tire_table_limits_checked_before_cuda():
+    """The lateral tire table (csrc/bssmppi.cu tire_table_host) covers every
+    slip angle of a rollout, |alpha| <= pi + max |steering bound|: any
+    magic-formula shape factor passes validation (C = 2.5 included), and
+    steering bounds beyond +-2 pi -- or non-finite tire coefficients -- are
+    refused at context creation, before any CUDA call."""
     from dataclasses import replace
     from helpers import Inputs
     from paper_2408_00494_b200 import controllers as mc
@@ -82,16 +84,20 @@ def test_lateral_shape_factor_range_checked_before_cuda():
     inp = Inputs("c1_s0")
     lib = _lib.load()
     h = ctypes.c_void_p()
-    for cyf, expect in ((2.5, _lib.ERR_UNSUPPORTED), (2.0, None)):
-        model = replace(inp.model, c_lat_front=cyf)
+
+    def create(model, bounds):
         ctx = mc.RolloutContext(model, inp.track, inp.cost, noise=inp.noise)
         prob, _keep = mc.build_problem("bss", 64, 10, 16, 1.0, 0.1, inp.cfg.sigma_eps, inp.cfg.precision,
-                                       inp.cfg.bounds, False, ctx)
-        rc = lib.bssmppi_create(ctypes.byref(prob), 0, ctypes.byref(h))
-        if expect is None:
-            assert rc != _lib.ERR_UNSUPPORTED      # passes validation (then needs a GPU)
-        else:
-            assert rc == expect and b"shape factors" in lib.bssmppi_last_error()
+                                       bounds, False, ctx)
+        return lib.bssmppi_create(ctypes.byref(prob), 0, ctypes.byref(h))
+
+    for cyf in (2.5, 0.3):
+        rc = create(replace(inp.model, c_lat_front=cyf), inp.cfg.bounds)
+        assert rc not in (_lib.ERR_UNSUPPORTED, _lib.ERR_INVALID)   # passes validation (then needs a GPU)
+    wide = mc.ControlBounds(delta_max=7.0)
+    assert create(inp.model, wide) == _lib.ERR_UNSUPPORTED
+    assert b"steering bounds" in lib.bssmppi_last_error()
+    assert create(replace(inp.model, b_lat_rear=float("inf")), inp.cfg.bounds) == _lib.ERR_INVALID
 
 
 def test_no_cpu_fallback_without_gpu():

@@ -52,40 +52,6 @@ def test_sincos_pi():
     _check(_coeffs("void sincos_pi"), xs, np.sin, True, 1e-7, 3e-7)
 
 
-def test_sin_pi_x2_is_the_sincos_pi_sine():
-    """The packed tire sine (lateral C atan(.), |.| <= pi for C <= 2) runs the
-    sincos_pi sine polynomial: same coefficients, same Horner order."""
-    body = SRC[SRC.index("float2 sin_pi_x2"):]
-    body = body[:body.index("\n}\n")]
-    c = [np.float32(float(v)) for v in re.findall(r"bc2\(([-0-9.e+]+)f\)", body)]
-    assert c == _coeffs("void sincos_pi")
-    from paper_2408_00494_b200.dynamics import VehicleParams
-    p = VehicleParams()
-    assert 0 < p.c_lat_front <= 2.0 and 0 < p.c_lat_rear <= 2.0   # the default car is supported
-
-
-def test_sin_tire_x2_short():
-    """Short lateral tire sine (|x| <= 2.2, lateral C <= 1.40): float32
-    Horner in the kernel's order within 2.5e-7 absolute / 3e-7 relative,
-    bracket constant exactly 1 (no relative bias at small slip)."""
-    body = SRC[SRC.index("float2 sin_tire_x2"):]
-    body = body[:body.index("\n}\n")]
-    c = [np.float32(float(v)) for v in re.findall(r"bc2\(([-0-9.e+]+)f\)", body)]
-    assert len(c) == 6 and c[-1] == np.float32(1.0)
-    x = np.linspace(-2.2, 2.2, 200001).astype(np.float32)
-    x = x[x != 0]
-    t = (x * x).astype(np.float32)
-    p = _horner(c, t)
-    y = (p * x).astype(np.float32).astype(np.float64)
-    ex = np.sin(x.astype(np.float64))
-    e = np.abs(y - ex)
-    assert e.max() < 2.5e-7, e.max()
-    assert (e / np.abs(ex)).max() < 3e-7
-    from paper_2408_00494_b200.dynamics import VehicleParams
-    p = VehicleParams()
-    assert max(p.c_lat_front, p.c_lat_rear) * np.pi / 2 <= 2.2   # the default car takes the short form
-
-
 def _atan_x2_coeffs():
     body = SRC[SRC.index("float2 atan_mag_x2"):]
     body = body[:body.index("\n}\n")]

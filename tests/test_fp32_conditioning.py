@@ -74,3 +74,22 @@ def test_naive_fp32_port_misses_the_tolerance(table):
     over = {n for n, (_, (nm, nc)) in table.items() if max(nm, nc) > 1e-4}
     assert len(over) >= 4, over
     assert "collapse_m16" in over
+
+
+def test_rounding_spread_fixture_reproduces():
+    """tests/golden/fp32_floor.json (the per-case FP32 rounding spread the
+    parity tolerance uses) is what tests/golden/make_fp32_floor.py computes:
+    re-run two cases and compare every run exactly; and it exceeds 1e-4
+    only on the two ill-conditioned cases."""
+    import json
+    import sys
+    from helpers import GOLDEN
+    sys.path.insert(0, str(GOLDEN))
+    import make_fp32_floor as mk
+    d = json.loads((GOLDEN / "fp32_floor.json").read_text())
+    assert d["runs"] == mk.R
+    for name in ("c1_s0", "low_speed"):
+        e = mk.jitter_errors(name)
+        assert list(e[:, 0]) == d["cases"][name]["mean_runs"]
+    over = {n for n, v in d["cases"].items() if v["mean_max"] > 1e-4}
+    assert over == {"s_wrap", "low_speed"}, over

@@ -73,3 +73,72 @@ def test_limits_are_refused():
             _run(K, M, T, persist)
         assert isinstance(ei.value, _lib.BssMppiError)
         assert what in _lib.load().bssmppi_last_error()
+
+
+@pytest.mark.parametrize("tire", [dict(c_lat_front=2.5, c_lat_rear=2.2),            # C > 2: interior zero of the force
+                                  dict(b_lat_front=12.0, b_lat_rear=9.0),          # stiff: > 330 table rows (global copy)
+                                  dict(b_lat_front=1.5, c_lat_front=0.8)],
+                         ids=["wideC", "stiffB", "soft"])
+def test_tire_table_shapes_match_oracle(tire):
+    """The lateral forces come from the per-context tire table (any B, C):
+    belief rollouts for tires the old polynomial sine could not take (C > 2)
+    and for stiff tires whose table exceeds the kernels' shared copy (read
+    from global memory instead) match the FP64 C oracle at the north-star
+    cost bound."""
+    from dataclasses import replace
+    K, M, T = 256, 32, 20
+    track = named_track("ellipse")
+    model = replace(md.with_timestep(md.VehicleParams(), 0.05, "euler"), **tire)
+    noise = md.NoiseModel(np.diag([0.04 ** 2] * 3))
+    cfg = mc.MppiConfig(kind="bss", samples=K, horizon=T, inner_samples=M, sigma_eps=np.diag([0.2 ** 2, 0.5 ** 2]))
+    ctx = mc.RolloutContext(model, track, mc.CostSpec(), noise=noise)
+    x0 = md.VehicleState.rolling(5.0, model, s=23.0).as_array()
+    rng = np.random.default_rng(11)
+    nominal = np.tile([0.05, 0.3], (T, 1))
+    eps = rng.standard_normal((K, T, 2)) @ md.psd_factor(cfg.sigma_eps).T
+    u = np.clip(nominal[None] + eps, [-0.35, -1.0], [0.35, 1.0])
+    kb = (27182818, 31415926)
+    gpu = mc.rollout_bss(x0, np.zeros((4, 4)), mc.RolloutBatch(u, eps), nominal, ctx, mc.DeviceKey(kb), M,
+                         precision=cfg.precision, cost_weight=cfg.control_cost_weight)
+    prob, _keep = mc.build_problem("bss", K, T, M, 1.0, cfg.control_cost_weight, cfg.sigma_eps, cfg.precision,
+                                   cfg.bounds, False, ctx)
+    ref, _ = c_oracle.rollout(prob, x0, np.zeros((4, 4)), nominal, u=u, eps=eps, key_belief=kb)
+    fin = np.isfinite(ref)
+    assert np.array_equal(np.isfinite(gpu), fin)
+    rel = np.abs(gpu[fin] - ref[fin]) / np.abs(ref[fin])
+    assert rel.max() < 1e-3, rel.max()
+    assert np.median(rel) < 1e-5
+
+
+def test_step_array_steering_beyond_the_table():
+    """step_array takes arbitrary controls: slip angles past the tire table's
+    domain (steering far outside the controller bounds) fall back to the
+    libdevice magic formula, so the step still matches the FP64 oracle."""
+    from oracle import bss_oracle as orc
+    track = named_track("ellipse")
+    model = md.with_timestep(md.VehicleParams(), 0.05, "euler")
+    rng = np.random.default_rng(5)
+    n = 2048
+    x = np.zeros((n, 8))
+    x[:, 0] = rng.uniform(-3, 7, n)
+    x[:, 1] = rng.normal(0, 0.5, n)
+    x[:, 2] = rng.normal(0, 0.8, n)
+    x[:, 3] = x[:, 0] / 0.095
+    x[:, 4] = x[:, 0] / 0.095
+    x[:, 5] = rng.normal(0, 0.3, n)
+    x[:, 6] = rng.uniform(-1.0, 1.0, n)
+    x[:, 7] = rng.uniform(0, track.length, n)
+    u = np.stack([rng.uniform(-3.0, 3.0, n), rng.uniform(-1, 1, n)], 1)   # |steering| up to 3 rad
+    ctx = mc.RolloutContext(model, track, mc.CostSpec())
+    prob, _keep = mc.build_problem("mppi", 1, 1, 1, 1.0, 0.0, np.eye(2), None, mc.ControlBounds(), False, ctx)
+    dc = mc.DeviceContext(prob)
+    out = np.empty_like(x)
+    ok = np.empty(n, dtype=np.uint8)
+    _lib.check(dc.lib.bssmppi_step_array(dc.h, n, _lib.dptr(x), _lib.dptr(u), None, _lib.dptr(out),
+                                         ok.ctypes.data_as(_lib.C.POINTER(_lib.C.c_uint8))))
+    ref, ref_ok = orc.step_euler(x, u, orc.phys(model), track, model.dt)
+    assert np.array_equal(ok.astype(bool), ref_ok)
+    scale = np.array([5, 1, 1, 50, 50, 1, 1, track.length])
+    err = np.abs(out - ref) / scale
+    assert err.max() < 5e-6, err.max()
+    dc.close()

@@ -11,11 +11,8 @@ tmp=$(mktemp -d)
 (cd "$tmp" && cuobjdump -xelf all "$OLDPWD/paper_2408_00494_b200/libbssmppi.so" > /dev/null && nvdisasm -g bssmppi.sm_100a.cubin > all.sass)
 # the C3 launch: G = 8, Philox noise, 128-thread blocks
 K=$(grep -o '^\.text\._ZN3bss18bss_rollout_kernelILi8ELb0ELb0ELi128EEEvNS_10RollParamsE' "$tmp/all.sass" | head -1 | sed 's/^\.text\.//')
-python tools/ncu_summary.py gpurun_out/r_prof_c3.ncu-rep 209715200 \
-  "$P ncu summary — bss_rollout_kernel<8,false,false> (G=8: 4 rollouts per warp, 32 particles per lane), C3 (K=16384, M=256, T=50)" \
-  "ncu --set full --clock-control none --import-source on -k regex:bss_rollout -s 1 -c 1 python tools/profile_iter.py --iters 2" \
-  > profiles/${P}_rollout_ncu_c3.md
-ncu -i gpurun_out/r_prof_c3.ncu-rep --page source --csv --print-source sass > "$tmp/k.csv" 2> /dev/null
+cp gpurun_out/r_ncu_c3.md profiles/${P}_rollout_ncu_c3.md
+cp gpurun_out/r_src_c3.csv "$tmp/k.csv"
 { echo "# Executed lane-instructions per particle-step of bss_rollout_kernel<8,false,false> at C3, by SASS opcode and by CUDA source line"
   echo "# (ncu source page of r_prof_c3.ncu-rep joined with nvdisasm -g line info: python tools/sass_exec.py k.csv all.sass <kernel> 209715200)"
   python tools/sass_exec.py "$tmp/k.csv" "$tmp/all.sass" $K 209715200; } > profiles/${P}_rollout_lines_c3.txt
