@@ -353,6 +353,7 @@ __device__ __forceinline__ float tire_q(float a, const VehDev &V, int axle) {
   const float nf = fmaf(a, V.tire_s, MAGIC);
   const float f = fmaf(a, V.tire_s, -(nf - MAGIC));
   const uint32_t j = __float_as_uint(nf) & 0x7ffu;
+  BSS_ASSERT(j < (uint32_t)V.tire_rows && (!TS || j < (uint32_t)kTireSmemRows));
   float4 c;
   if (TS) c = g_tire_tab[axle * kTireSmemRows + j];
   else c = __ldg(V.tire + axle * V.tire_rows + j);

@@ -1,0 +1,6 @@
+# The GPU suite against the bounds-checked build (-DBSS_CHECKED: device
+# asserts on array, table and noise indices).
+mkdir -p gpurun_out
+BSSMPPI_LIB=$PWD/paper_2408_00494_b200/libbssmppi_checked.so timeout 2400 python -m pytest tests -q -m gpu -p no:cacheprovider -k "not acceptance" > gpurun_out/pytest_checked.log 2>&1
+echo "rc=$?" >> gpurun_out/pytest_checked.log
+tail -4 gpurun_out/pytest_checked.log
