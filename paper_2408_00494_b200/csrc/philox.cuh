@@ -154,23 +154,45 @@ __device__ __forceinline__ float2 angle_entry(uint32_t j) {
 // LDS carries its offset as an immediate.
 __shared__ __align__(16) float2 g_angle_tab[kAngleTab];
 
+// 32-bit shared-window address of a table, made opaque to the compiler: a
+// per-thread register computed once per (k, t) instead of a uniform-register
+// window base the compiler rebuilds (S2UR / UMOV / ULEA) inside the loop.
+__device__ __forceinline__ uint32_t opaque_u32(uint32_t v) {
+  asm volatile("" : "+r"(v));
+  return v;
+}
+__device__ __forceinline__ uint32_t angle_tab_addr() {
+  return opaque_u32((uint32_t)__cvta_generic_to_shared(g_angle_tab));
+}
+__device__ __forceinline__ float2 angle_lds(uint32_t base, uint32_t w) {
+  float2 v;
+  asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(base + ((w & 0xfffu) << 3)));
+  return v;
+}
+__device__ __forceinline__ float angle_lds_x(uint32_t base, uint32_t w) {
+  float v;
+  asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(base + ((w & 0xfffu) << 3)));
+  return v;
+}
+
+// base: angle_tab_addr() of the calling block (TAB only)
 template <bool TAB>
-__device__ __forceinline__ float2 angle_cs(uint32_t w) {
-  if (TAB) return g_angle_tab[w & 0xfffu];
+__device__ __forceinline__ float2 angle_cs(uint32_t w, uint32_t base) {
+  if (TAB) return angle_lds(base, w);
   return angle_entry(w & 0xfffu);
 }
 
 template <bool TAB>
-__device__ __forceinline__ void box_muller_word(uint32_t w, float &z0, float &z1) {
+__device__ __forceinline__ void box_muller_word(uint32_t w, float &z0, float &z1, uint32_t base = 0) {
   const float r = word_radius(w);
-  const float2 cs = angle_cs<TAB>(w);
+  const float2 cs = angle_cs<TAB>(w, base);
   const float2 z = __fmul2_rn(make_float2(r, r), cs);
   z0 = z.x;
   z1 = z.y;
 }
 template <bool TAB>
-__device__ __forceinline__ void box_muller_word1(uint32_t w, float &z0) {
-  z0 = word_radius(w) * (TAB ? g_angle_tab[w & 0xfffu].x : angle_entry(w & 0xfffu).x);
+__device__ __forceinline__ void box_muller_word1(uint32_t w, float &z0, uint32_t base = 0) {
+  z0 = word_radius(w) * (TAB ? angle_lds_x(base, w) : angle_entry(w & 0xfffu).x);
 }
 
 __host__ __device__ __forceinline__ Philox4 belief_block(const PhiloxKeys &rk, uint32_t t, uint32_t kg, uint32_t m) {
@@ -235,7 +257,7 @@ __device__ __forceinline__ float radius_mantissa(uint32_t w, uint32_t one_bits) 
 // word_radius / box_muller_word arithmetic with the four uniforms formed
 // as two FADD2 pairs.
 template <bool TAB>
-__device__ __forceinline__ void raw_normals_from_block(const Philox4 &a, float z[7]) {
+__device__ __forceinline__ void raw_normals_from_block(const Philox4 &a, float z[7], uint32_t base = 0) {
 #ifdef __CUDA_ARCH__
   uint32_t one;
   asm("mov.b32 %0, 0x3f800000;" : "=r"(one));
@@ -245,16 +267,16 @@ __device__ __forceinline__ void raw_normals_from_block(const Philox4 &a, float z
                                 make_float2(-radius_mantissa(a.z, one), -radius_mantissa(a.w, one)));
   const float r0 = sqrt_approx(-lg2_approx(u01.x)), r1 = sqrt_approx(-lg2_approx(u01.y));
   const float r2 = sqrt_approx(-lg2_approx(u23.x)), r3 = sqrt_approx(-lg2_approx(u23.y));
-  const float2 p0 = __fmul2_rn(make_float2(r0, r0), angle_cs<TAB>(a.x));
-  const float2 p1 = __fmul2_rn(make_float2(r1, r1), angle_cs<TAB>(a.y));
-  const float2 p2 = __fmul2_rn(make_float2(r2, r2), angle_cs<TAB>(a.z));
+  const float2 p0 = __fmul2_rn(make_float2(r0, r0), angle_cs<TAB>(a.x, base));
+  const float2 p1 = __fmul2_rn(make_float2(r1, r1), angle_cs<TAB>(a.y, base));
+  const float2 p2 = __fmul2_rn(make_float2(r2, r2), angle_cs<TAB>(a.z, base));
   z[0] = p0.x; z[1] = p0.y; z[2] = p1.x; z[3] = p1.y; z[4] = p2.x; z[5] = p2.y;
-  z[6] = r3 * (TAB ? g_angle_tab[a.w & 0xfffu].x : angle_entry(a.w & 0xfffu).x);
+  z[6] = r3 * (TAB ? angle_lds_x(base, a.w) : angle_entry(a.w & 0xfffu).x);
 #else
-  box_muller_word<TAB>(a.x, z[0], z[1]);
-  box_muller_word<TAB>(a.y, z[2], z[3]);
-  box_muller_word<TAB>(a.z, z[4], z[5]);
-  box_muller_word1<TAB>(a.w, z[6]);
+  box_muller_word<TAB>(a.x, z[0], z[1], base);
+  box_muller_word<TAB>(a.y, z[2], z[3], base);
+  box_muller_word<TAB>(a.z, z[4], z[5], base);
+  box_muller_word1<TAB>(a.w, z[6], base);
 #endif
 }
 
@@ -279,9 +301,10 @@ __device__ __forceinline__ float centred_uniform2_16(uint32_t field_at_top) {
 
 // z[0:4] are RAW normals (x kBmNeg = standard), w the noise increments.
 template <bool TAB>
-__device__ __forceinline__ void laplace_from_block(const Philox4 &p, float b, float a, float z[4], float w[3]) {
-  box_muller_word<TAB>(p.x, z[0], z[1]);
-  box_muller_word<TAB>(p.y, z[2], z[3]);
+__device__ __forceinline__ void laplace_from_block(const Philox4 &p, float b, float a, float z[4], float w[3],
+                                                   uint32_t base = 0) {
+  box_muller_word<TAB>(p.x, z[0], z[1], base);
+  box_muller_word<TAB>(p.y, z[2], z[3], base);
   const uint32_t fields[4] = {p.z & 0xffff0000u, p.z << 16, p.w & 0xffff0000u, p.w << 16};
 #pragma unroll
   for (int i = 0; i < 3; ++i) {

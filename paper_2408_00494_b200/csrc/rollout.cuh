@@ -301,6 +301,53 @@ __device__ __forceinline__ void group_allreduce18(float a[18], int li, float *sl
   a[17] = v.y;
 }
 
+// The same for the 16 sums of re-projected particles (the two wheel-speed
+// sums are identically zero and skipped): exact halvings at every level, so
+// G = 32 needs 16 shuffles instead of 20 (and half the selects); the last
+// level of G = 32 pairs lanes holding one value each (both keep the sum).
+template <int G>
+__device__ __forceinline__ void group_allreduce16(float a[16], int li, float *slot) {
+  int base = 0;
+#define BSS_RS16(N, OFF)                                                       \
+  {                                                                            \
+    constexpr int H = N / 2;                                                   \
+    const bool up = (li & OFF) != 0;                                           \
+    _Pragma("unroll") for (int i = 0; i < H; ++i) {                            \
+      const float send = up ? a[i] : a[i + H];                                 \
+      const float keep = up ? a[i + H] : a[i];                                 \
+      a[i] = keep + __shfl_xor_sync(0xffffffffu, send, OFF);                   \
+    }                                                                          \
+    base += up ? H : 0;                                                        \
+  }
+  if (G == 32) {
+    BSS_RS16(16, 16) BSS_RS16(8, 8) BSS_RS16(4, 4) BSS_RS16(2, 2)
+    a[0] += __shfl_xor_sync(0xffffffffu, a[0], 1);
+    if ((li & 1) == 0) slot[base] = a[0];
+  } else if (G == 16) {
+    BSS_RS16(16, 8) BSS_RS16(8, 4) BSS_RS16(4, 2) BSS_RS16(2, 1)
+    slot[base] = a[0];
+  } else if (G == 8) {
+    BSS_RS16(16, 4) BSS_RS16(8, 2) BSS_RS16(4, 1)
+    slot[base] = a[0]; slot[base + 1] = a[1];
+  } else if (G == 4) {
+    BSS_RS16(16, 2) BSS_RS16(8, 1)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) slot[base + i] = a[i];
+  } else {  // G == 2
+    BSS_RS16(16, 1)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) slot[base + i] = a[i];
+  }
+#undef BSS_RS16
+  __syncwarp();
+  const float4 *s4 = reinterpret_cast<const float4 *>(slot);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float4 v = s4[i];
+    a[4 * i] = v.x; a[4 * i + 1] = v.y; a[4 * i + 2] = v.z; a[4 * i + 3] = v.w;
+  }
+}
+
 constexpr int kSlotFloats = 20;   // 18 sums, 16-byte aligned slot
 #ifndef BSS_BLOCK_THREADS
 #define BSS_BLOCK_THREADS 128
@@ -378,7 +425,7 @@ enum NoiseKind { NK_GAUSS_DIAG = 0, NK_LAPLACE = 1, NK_GAUSS_GENERAL = 2 };
 // of particle_pass is one branch-free scheduling region.
 template <bool ZARR, int NK, bool TAB>
 __device__ __forceinline__ void particle_noise(const RollParams &P, const BeliefPrefix &bp,
-                                               int t, int k, int m, float n[7]) {
+                                               int t, int k, int m, float n[7], uint32_t ang) {
   if (ZARR) {
     if (m < P.M) {
       BSS_ASSERT(t < P.T && k < P.k_count);
@@ -391,8 +438,8 @@ __device__ __forceinline__ void particle_noise(const RollParams &P, const Belief
     }
   } else {
     const Philox4 a = belief_block_m(bp, P.kb, (uint32_t)m);
-    if (NK == NK_LAPLACE) laplace_from_block<TAB>(a, P.lap_b, P.slip_a, n, n + 4);
-    else raw_normals_from_block<TAB>(a, n);
+    if (NK == NK_LAPLACE) laplace_from_block<TAB>(a, P.lap_b, P.slip_a, n, n + 4, ang);
+    else raw_normals_from_block<TAB>(a, n, ang);
   }
 }
 
@@ -401,7 +448,7 @@ __device__ __forceinline__ void particle_noise(const RollParams &P, const Belief
 template <bool PERSIST, bool ZARR, int NK, bool TS>
 __device__ __forceinline__ void particle_step(const RollParams &P, int t, int m, const float mean[8],
                                               const float L[10], const CtlDev &ctl, const StepShared &sh,
-                                              float *cloud, const float z[7], float x[8]) {
+                                              float *cloud, const float z[7], float x[8], uint32_t tire) {
   const int M = P.M;
   const float *F = ZARR ? P.F : P.Fk;   // Philox normals arrive raw (x kBmNeg folded in)
   if (PERSIST && t > 0) {
@@ -426,7 +473,7 @@ __device__ __forceinline__ void particle_step(const RollParams &P, int t, int m,
   // per-particle ok is discarded (belief.py:370); a re-projected particle
   // shares (vx, omega_f, omega_r, s) with the mean, hence the shared terms
   if (PERSIST && t > 0) vehicle_step<TS>(x, ctl, P.V, P.tr);
-  else step_particle<TS>(x, sh, ctl, P.V, P.tr);
+  else step_particle<TS>(x, sh, ctl, P.V, P.tr, tire);
   if (NK == NK_LAPLACE) {                // config-4 extension, after integration too
     x[0] += z[4];
     x[1] += z[5];
@@ -523,9 +570,12 @@ __device__ __forceinline__ void particle_pass(const RollParams &P, int t, int k,
   float x[8], zc[7], zn[7];
   // Philox rounds 0-2 minus the particle index: once per (k, t)
   const BeliefPrefix bp = ZARR ? BeliefPrefix{} : belief_prefix(P.kb, (uint32_t)t, (uint32_t)kg);
-  particle_noise<ZARR, NK, TAB>(P, bp, t, k, li, zc);
-  if (li + G < M) particle_noise<ZARR, NK, TAB>(P, bp, t, k, li + G, zn);
-  if (has0) particle_step<PERSIST, ZARR, NK, TS>(P, t, li, mean, L, ctl, sh, cloud, zc, x);
+  // table addresses in registers for the loop (philox.cuh opaque_u32)
+  const uint32_t ang = TAB && !ZARR ? angle_tab_addr() : 0u;
+  const uint32_t tire = TS ? tire_tab_addr() : 0u;
+  particle_noise<ZARR, NK, TAB>(P, bp, t, k, li, zc, ang);
+  if (li + G < M) particle_noise<ZARR, NK, TAB>(P, bp, t, k, li + G, zn, ang);
+  if (has0) particle_step<PERSIST, ZARR, NK, TS>(P, t, li, mean, L, ctl, sh, cloud, zc, x, tire);
 #pragma unroll
   for (int i = 0; i < 8; ++i) c[i] = __shfl_sync(0xffffffffu, x[i], 0, G);
   // persist clouds need the wheel sums too (scalar form); re-projected
@@ -544,12 +594,12 @@ __device__ __forceinline__ void particle_pass(const RollParams &P, int t, int k,
   for (; m + G < M; m += G) {             // steady state: look one particle ahead
 #pragma unroll
     for (int j = 0; j < 7; ++j) zc[j] = zn[j];
-    particle_noise<ZARR, NK, TAB>(P, bp, t, k, m + G, zn);
-    particle_step<PERSIST, ZARR, NK, TS>(P, t, m, mean, L, ctl, sh, cloud, zc, x);
+    particle_noise<ZARR, NK, TAB>(P, bp, t, k, m + G, zn, ang);
+    particle_step<PERSIST, ZARR, NK, TS>(P, t, m, mean, L, ctl, sh, cloud, zc, x, tire);
     add(x);
   }
   if (m < M) {                            // last particle: no look-ahead draw
-    particle_step<PERSIST, ZARR, NK, TS>(P, t, m, mean, L, ctl, sh, cloud, zn, x);
+    particle_step<PERSIST, ZARR, NK, TS>(P, t, m, mean, L, ctl, sh, cloud, zn, x, tire);
     add(x);
   }
   if (!PERSIST) unpack_acc(A, acc);
@@ -621,7 +671,17 @@ __device__ __forceinline__ void bss_rollout(const RollParams &P) {
     float c[8];
     particle_pass<G, PERSIST, ZARR, NK, TS>(P, t, k, kg, li, mean, L, ctl, sh, cloud, acc, c);
     if (t + 1 < P.T) cv = ctl_row[t + 1];
-    group_allreduce18<G>(acc, li, slots + (t & 1) * kSlotFloats);
+    if (PERSIST) {
+      group_allreduce18<G>(acc, li, slots + (t & 1) * kSlotFloats);
+    } else {   // wheel sums are zero after re-projection: reduce the other 16
+      float a16[16] = {acc[0], acc[1], acc[2], acc[5], acc[6], acc[7], acc[8], acc[9],
+                       acc[10], acc[11], acc[12], acc[13], acc[14], acc[15], acc[16], acc[17]};
+      group_allreduce16<G>(a16, li, slots + (t & 1) * kSlotFloats);
+      acc[0] = a16[0]; acc[1] = a16[1]; acc[2] = a16[2]; acc[3] = 0.f; acc[4] = 0.f;
+      acc[5] = a16[3]; acc[6] = a16[4]; acc[7] = a16[5];
+#pragma unroll
+      for (int i = 8; i < 18; ++i) acc[i] = a16[i - 2];
+    }
 
     // moments (belief.py:275-308 semantics)
     float mu[8], dm[8];

@@ -193,11 +193,15 @@ __device__ __forceinline__ bool finite6(const float x[8]) {
 // component.  True only if neither can occur: 0 <= s < L (both the floor-mod
 // and the clamp are the identity there) and the other components finite
 // (their max.NaN is below inf).  Compares and max chains only -- ALU work,
-// no FMA-pipe cycle -- feeding one branch.  The heading wrap keeps its own
-// early test (wrap_pi): folding it in as well measured slower (profiles/).
+// no FMA-pipe cycle -- feeding one branch.  The particle step adds the
+// heading-wrap test to the same screen (common_case_psi below; round 1
+// measured the merge slower, the round-2 kernel 1.5% faster, profiles/).
 __device__ __forceinline__ bool common_case(const float x[8], const TrackDev &tr) {
   const float m = max3_nan(max3_nan(fabsf(x[0]), fabsf(x[1]), fabsf(x[2])), fabsf(x[6]), fabsf(x[5]));
-  return (m < __int_as_float(0x7f800000)) & (x[7] >= 0.f) & (x[7] < tr.L);
+  // 0 <= s < L as ONE unsigned compare of the bit patterns (L > 0: for
+  // non-negative floats the order is the integers'; negative s, -0 and NaN
+  // compare above L's pattern and take the exact path, which keeps -0)
+  return (m < __int_as_float(0x7f800000)) & (__float_as_uint(x[7]) < __float_as_uint(tr.L));
 }
 
 // The exact per-component treatment when common_case fails: arc-length
@@ -205,6 +209,17 @@ __device__ __forceinline__ bool common_case(const float x[8], const TrackDev &tr
 __device__ __forceinline__ bool rare_fixup(float x[8], const TrackDev &tr) {
   x[7] = track_s(x[7], tr);
   return finite6(x) || scrub_nonfinite6(x);
+}
+
+// common_case plus |e_psi| < pi (the heading wrap is the identity there),
+// and the fix-up in the reference's order: heading wrap (dynamics.py:486),
+// arc length, non-finite scrub.
+__device__ __forceinline__ bool common_case_psi(const float x[8], const TrackDev &tr) {
+  return common_case(x, tr) & (fabsf(x[5]) < 3.14159265358979f);
+}
+__device__ __forceinline__ bool rare_fixup_psi(float x[8], const TrackDev &tr) {
+  x[5] = wrap_pi(x[5]);
+  return rare_fixup(x, tr);
 }
 
 // The step split in two: everything that depends only on (vx, omega_f,
@@ -304,7 +319,7 @@ __device__ __forceinline__ StepShared step_shared(const float x[8], const CtlDev
 // libdevice reference form (A/B parity builds, build_cuda(exact=True)).
 template <bool TS = false>
 __device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, const CtlDev &c,
-                                              const VehDev &V, const TrackDev &tr) {
+                                              const VehDev &V, const TrackDev &tr, uint32_t tire_base = 0) {
   const float vx = x[0], vy = x[1], r = x[2], ep = x[5], ey = x[6], s = x[7];
   const float af = c.delta - atan2f(vy + V.lf * r, h.vxe);
   const float ar = -atan2f(vy - V.lr * r, h.vxe);
@@ -344,8 +359,15 @@ __device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, c
 // 1.5 2^23 rounding trick (the row number ends up in the low mantissa bits,
 // no F2I), the in-cell offset by one FFMA, the cubic by three.  NaN / inf
 // arguments read row 0 and propagate through f.
+__device__ __forceinline__ uint32_t tire_tab_addr() {
+  uint32_t v = (uint32_t)__cvta_generic_to_shared(g_tire_tab);
+  asm volatile("" : "+r"(v));   // opaque: kept in a register (philox.cuh opaque_u32)
+  return v;
+}
+
+// base: tire_tab_addr() of the calling block (TS only)
 template <bool TS>
-__device__ __forceinline__ float tire_q(float a, const VehDev &V, int axle) {
+__device__ __forceinline__ float tire_q(float a, const VehDev &V, int axle, uint32_t base) {
   const float MAGIC = 12582912.0f;   // 1.5 2^23
   if (!TS) {   // step kernels: arbitrary steering; keep the row in range (NaN stays NaN)
     asm("min.NaN.f32 %0, %0, %1;" : "+f"(a) : "f"(V.tire_amax));
@@ -355,7 +377,10 @@ __device__ __forceinline__ float tire_q(float a, const VehDev &V, int axle) {
   const uint32_t j = __float_as_uint(nf) & 0x7ffu;
   BSS_ASSERT(j < (uint32_t)V.tire_rows && (!TS || j < (uint32_t)kTireSmemRows));
   float4 c;
-  if (TS) c = g_tire_tab[axle * kTireSmemRows + j];
+  if (TS) {
+    asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(c.x), "=f"(c.y), "=f"(c.z), "=f"(c.w)
+        : "r"(base + (uint32_t)(axle * kTireSmemRows * 16) + (j << 4)));
+  }
   else c = __ldg(V.tire + axle * V.tire_rows + j);
   return fmaf(fmaf(fmaf(c.w, f, c.z), f, c.y), f, c.x);
 }
@@ -365,8 +390,8 @@ __device__ __forceinline__ float tire_q(float a, const VehDev &V, int axle) {
 // steering is clamped to its bounds, which size the table); the step kernels
 // also take arbitrary steering and fall back to libdevice beyond it.
 template <bool TS>
-__device__ __forceinline__ float2 lateral_shape(float2 al, const VehDev &V) {
-  const float2 q = make_float2(tire_q<TS>(fabsf(al.x), V, 0), tire_q<TS>(fabsf(al.y), V, 1));
+__device__ __forceinline__ float2 lateral_shape(float2 al, const VehDev &V, uint32_t base) {
+  const float2 q = make_float2(tire_q<TS>(fabsf(al.x), V, 0, base), tire_q<TS>(fabsf(al.y), V, 1, base));
   float2 g = __fmul2_rn(al, q);
   if (!TS && __builtin_expect(fmaxf(fabsf(al.x), fabsf(al.y)) > V.tire_amax, 0)) {
     if (fabsf(al.x) > V.tire_amax) g.x = sinf(V.Cyf * atanf(V.Byf * al.x));
@@ -383,7 +408,7 @@ __device__ __forceinline__ float2 lateral_shape(float2 al, const VehDev &V) {
 // TS: the tire table is the belief kernel's shared copy (else global memory).
 template <bool TS = false>
 __device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, const CtlDev &c,
-                                              const VehDev &V, const TrackDev &tr) {
+                                              const VehDev &V, const TrackDev &tr, uint32_t tire_base = 0) {
   const float vx = x[0], vy = x[1], r = x[2], ep = x[5], ey = x[6], s = x[7];
   // slip-angle numerators (vy + lf r, vy - lr r); atan2(., vxe) = atan(. / vxe)
   // for vxe > 0, +-pi shifted for vxe < 0 (vxe is shared by the rollout)
@@ -394,7 +419,7 @@ __device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, c
   const float2 A = atan2_x2(__fmul2_rn(Y, bc2(h.rx)), Y, h.rev);
   // slip angles alpha_f = delta - A.x, alpha_r = -A.y; lateral forces
   // D |cos|_long sin(C atan(B alpha)) from the tire table
-  const float2 fy = __fmul2_rn(h.dycx, lateral_shape<TS>(make_float2(c.delta - A.x, -A.y), V));
+  const float2 fy = __fmul2_rn(h.dycx, lateral_shape<TS>(make_float2(c.delta - A.x, -A.y), V, tire_base));
   // body-frame front force + rear longitudinal: (fxf cd - fyf sd + fxr, fxf sd + fyf cd)
   const float2 fb = __ffma2_rn(bc2(fy.x), h.nsd_cd, h.fb0);
   float frame = 1.f - h.kap * ey;
@@ -416,10 +441,13 @@ __device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, c
   x[2] = fmaf(V.dt_lf_iz, fb.y, fmaf(V.ndt_lr_iz, fy.y, r));   // r + dt (lf fyb - lr fyr) / Iz
   x[3] = h.wf1;
   x[4] = h.wr1;
-  x[5] = wrap_pi(v56.x);
+  x[5] = v56.x;   // wrapped in rare_fixup_psi (one screen for all rare events)
   x[6] = v56.y;
   x[7] = fmaf(V.dt, ds, s);
-  if (__builtin_expect(!common_case(x, tr), 0)) ok = rare_fixup(x, tr) && ok;
+  // one screen for all rare events: heading wrap, arc-length wrap / clamp,
+  // non-finite components (ALU compares, one branch; -1.5% at C3 against a
+  // separate early heading test, profiles/README.md)
+  if (__builtin_expect(!common_case_psi(x, tr), 0)) ok = rare_fixup_psi(x, tr) && ok;
   return ok && h.wfin;
 }
 #endif
