@@ -3,44 +3,14 @@
 // The libdevice versions (sinf/sincosf/atan2f/division) carry range
 // reduction and IEEE slow paths the particle step never needs; these keep
 // ~1-3 ulp accuracy on the ranges that occur and cost a handful of FMAs.
-// Coefficients are Lawson-iterated (minimax) least-squares fits: the atan
-// constants are `tools/fit_poly.py atan` output verbatim; the sin/cos ones
-// come from an earlier fit of the same kind (`tools/fit_poly.py sincos_pi`
-// reproduces them to within the pinned bounds, not bit for bit).
+// Coefficients are Lawson-iterated (minimax) least-squares fits
+// (`tools/fit_poly.py atan`, `sincos_half`).  The lateral magic formula is
+// not here: it comes from the per-vehicle table of vehicle.cuh tire_q.
 // tests/test_fastmath.py re-evaluates every polynomial in float32 (same
 // Horner order) against float64 and pins the error bounds.
 #pragma once
 
 namespace bss {
-
-// sin and cos on any x: reduced to [-pi, pi] (a no-op for heading errors,
-// which the step keeps in (-pi, pi]).
-__device__ __forceinline__ void sincos_pi(float x, float &s, float &c) {
-  if (fabsf(x) > 3.14159265f) {
-    const float n = rintf(x * 0.159154943f);
-    x = fmaf(-n, 6.28318548e+00f, x);
-    x = fmaf(n, 1.74845553e-07f, x);
-  }
-  const float t = x * x;
-  float p = -6.416872784e-13f;
-  p = fmaf(p, t, 1.582333015e-10f);
-  p = fmaf(p, t, -2.502759777e-08f);
-  p = fmaf(p, t, 2.755584774e-06f);
-  p = fmaf(p, t, -1.984121918e-04f);
-  p = fmaf(p, t, 8.333332837e-03f);
-  p = fmaf(p, t, -1.666666716e-01f);
-  p = fmaf(p, t, 1.0f);
-  s = p * x;
-  float q = 4.101670311e-14f;
-  q = fmaf(q, t, -1.134152147e-11f);
-  q = fmaf(q, t, 2.086320672e-09f);
-  q = fmaf(q, t, -2.755647870e-07f);
-  q = fmaf(q, t, 2.480155672e-05f);
-  q = fmaf(q, t, -1.388888806e-03f);
-  q = fmaf(q, t, 4.166666791e-02f);
-  q = fmaf(q, t, -5.0e-01f);
-  c = fmaf(q, t, 1.0f);
-}
 
 // ---- packed FP32x2 forms (sm_100 FFMA2/FMUL2/FADD2: two IEEE lanes per
 // issue slot, each lane rounded exactly like the scalar instruction).
@@ -124,13 +94,6 @@ __device__ __forceinline__ float2 sincos_pi_x2(float x) {
 #pragma unroll
   for (int j = 1; j < 6; ++j) p = __ffma2_rn(p, bc2(t), kSinCosHalf[j]);
   return make_float2(copysignf(p.x * h, x), b < a ? -p.y : p.y);
-}
-
-// atan2(y, x) given r = 1/x (x != 0, already computed by the caller):
-// atan(y r) in the right half plane, +-pi shifted in the left one.
-__device__ __forceinline__ float atan2_rcp(float y, float x, float r) {
-  const float a = atanf(y * r);
-  return x >= 0.f ? a : a + copysignf(3.14159265358979f, y);
 }
 
 // tanh(x); |x| >= 9.02 rounds to +-1 in FP32 (wheels at speed), which skips

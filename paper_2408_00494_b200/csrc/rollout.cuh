@@ -368,14 +368,6 @@ constexpr int kSmallBlockThreads = 64;
 #define BSS_MIN_BLOCKS 4
 #endif
 
-// Group-wide sum over G lanes (xor butterfly; every lane gets the total).
-template <int G>
-__device__ __forceinline__ float group_sum(float v) {
-#pragma unroll
-  for (int off = G / 2; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-  return v;
-}
-
 // Prologue shared by the rollout kernels: the G lanes of a group sample the
 // T controls of rollout k in parallel (lane l takes t = l, l+G, ...),
 // write the clamped u for the update and the per-(k,t) control table

@@ -13,43 +13,11 @@ SRC = (Path(__file__).resolve().parent.parent / "paper_2408_00494_b200" / "csrc"
        "fastmath.cuh").read_text()
 
 
-def _coeffs(func, var="p"):
-    body = SRC[SRC.index(func):]
-    body = body[:body.index("\n}\n")]
-    first = re.search(r"float %s = ([-0-9.e+]+)f;" % var, body).group(1)
-    rest = re.findall(r"%s = fmaf\(%s, t, ([-0-9.e+]+)f\);" % (var, var), body)
-    if var == "q":
-        rest.append("1.0")   # final c = fmaf(q, t, 1.0f)
-    return [np.float32(float(x)) for x in [first] + rest]
-
-
 def _horner(c, t):
     p = np.full_like(t, c[0])
     for ci in c[1:]:
         p = (p * t + ci).astype(np.float32)
     return p
-
-
-def _check(c, x, exact, odd, abs_tol, rel_tol=None):
-    x = x.astype(np.float32)
-    t = (x * x).astype(np.float32)
-    p = _horner(c, t)
-    y = (p * x).astype(np.float32) if odd else p
-    e = np.abs(y.astype(np.float64) - exact(x.astype(np.float64)))
-    assert e.max() < abs_tol, e.max()
-    if rel_tol is not None:
-        ex = np.abs(exact(x.astype(np.float64)))
-        big = ex > 1e-3
-        assert (e[big] / ex[big]).max() < rel_tol
-
-
-def test_sincos_pi():
-    x = np.linspace(-np.pi, np.pi, 200001)
-    _check(_coeffs("void sincos_pi"), x, np.sin, True, 5e-7)
-    _check(_coeffs("void sincos_pi", "q"), x, np.cos, False, 6e-7)
-    # heading errors are small in practice: near-ulp relative accuracy there
-    xs = np.linspace(-0.7, 0.7, 100001)
-    _check(_coeffs("void sincos_pi"), xs, np.sin, True, 1e-7, 3e-7)
 
 
 def _atan_x2_coeffs():
