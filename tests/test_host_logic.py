@@ -168,6 +168,45 @@ def test_reduce_scatter_schedule_covers_every_sum_once(G):
     assert np.allclose(slot, vals.sum(0))
 
 
+def _simulate_reduce_scatter16(G, vals):
+    # group_allreduce16: exact halvings, G = 32 ends with a pairwise add
+    levels = {32: [(16, 16), (8, 8), (4, 4), (2, 2)], 16: [(16, 8), (8, 4), (4, 2), (2, 1)],
+              8: [(16, 4), (8, 2), (4, 1)], 4: [(16, 2), (8, 1)], 2: [(16, 1)]}[G]
+    a = [list(v) for v in vals]
+    base = [0] * G
+    for N, OFF in levels:
+        H = N // 2
+        new = []
+        for lane in range(G):
+            up, p = bool(lane & OFF), lane ^ OFF
+            keep = a[lane][H:N] if up else a[lane][:H]
+            recv = a[p][H:N] if up else a[p][:H]       # what the partner sends
+            new.append([k + r for k, r in zip(keep, recv)])
+        for lane in range(G):
+            base[lane] += H if lane & OFF else 0
+        a = new
+    if G == 32:
+        a = [[a[lane][0] + a[lane ^ 1][0]] for lane in range(G)]
+    slot = [None] * 16
+    for lane in range(G):
+        if G == 32 and lane & 1:
+            continue
+        for i, v in enumerate(a[lane]):
+            assert slot[base[lane] + i] is None
+            slot[base[lane] + i] = v
+    return slot
+
+
+@pytest.mark.parametrize("G", [2, 4, 8, 16, 32])
+def test_reduce_scatter16_schedule_covers_every_sum_once(G):
+    """Host model of group_allreduce16 (csrc/rollout.cuh, the re-projection
+    path's 16 nonzero sums): every sum is written by exactly one lane and
+    equals the group sum."""
+    vals = np.random.default_rng(100 + G).normal(size=(G, 16))
+    slot = _simulate_reduce_scatter16(G, vals)
+    assert np.allclose(slot, vals.sum(0))
+
+
 class TestSharding:
     def test_partition(self):
         for K, W in [(16384, 8), (100, 3), (7, 7), (16384, 1)]:
