@@ -300,12 +300,9 @@ void fill_params(bssmppi_ctx *c, const bssmppi_problem *p) {
   V.rrf = (float)(q[19] * q[21] * q[4]); V.rrr = (float)(q[19] * q[22] * q[4]);
   V.spin_scale = (float)(q[4] / 0.1); V.dt = (float)p->dt;
   V.lf_nlr = make_float2(V.lf, -V.lr);
-  V.By_s = make_float2(V.Byf, -V.Byr);
-  V.nBy = make_float2(-V.Byf, -V.Byr);
   V.dt_lf_iz = (float)(p->dt * q[2] / q[1]);
   V.ndt_lr_iz = (float)(-p->dt * q[3] / q[1]);
   V.dt_m = (float)(p->dt / q[0]);
-  V.Cy = make_float2(V.Cyf, V.Cyr);
   V.Dy = make_float2(V.Dyf, V.Dyr);
   V.Bx = make_float2(V.Bxf, V.Bxr);
   V.Cx = make_float2(V.Cxf, V.Cxr);

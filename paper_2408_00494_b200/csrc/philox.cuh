@@ -147,11 +147,8 @@ __device__ __forceinline__ float2 angle_entry(uint32_t j) {
   return make_float2(c, s);
 }
 
-// TAB: read the block's shared-memory table, else evaluate in place
-// (statistics kernel, persist mode).
 // The table of a rollout block (filled by bss_rollout_kernel; kernels that
-// never name it do not allocate it).  Indexed through the symbol, so the
-// LDS carries its offset as an immediate.
+// never name it do not allocate it).
 __shared__ __align__(16) float2 g_angle_tab[kAngleTab];
 
 // 32-bit shared-window address of a table, made opaque to the compiler: a
@@ -175,7 +172,8 @@ __device__ __forceinline__ float angle_lds_x(uint32_t base, uint32_t w) {
   return v;
 }
 
-// base: angle_tab_addr() of the calling block (TAB only)
+// TAB: read the block's shared-memory table at base = angle_tab_addr(),
+// else evaluate in place (statistics kernel, persist mode).
 template <bool TAB>
 __device__ __forceinline__ float2 angle_cs(uint32_t w, uint32_t base) {
   if (TAB) return angle_lds(base, w);
@@ -255,7 +253,7 @@ __device__ __forceinline__ float radius_mantissa(uint32_t w, uint32_t one_bits) 
 
 // The 7 raw normals (standard normals / kBmNeg) of a particle-step: the
 // word_radius / box_muller_word arithmetic with the four uniforms formed
-// as two FADD2 pairs.
+// as two FADD2 pairs (the host pass of nvcc takes the scalar form).
 template <bool TAB>
 __device__ __forceinline__ void raw_normals_from_block(const Philox4 &a, float z[7], uint32_t base = 0) {
 #ifdef __CUDA_ARCH__

@@ -9,7 +9,8 @@
 //     particles (lane l handles m = l, l+G, ...); G is the power of two >= M
 //     (<= 32) narrowed by the measured policy in bssmppi.cu group_width
 //     (C3: G = 8, 4 rollouts per warp, 32 particles per lane); the only
-//     block-level sync is the one after the Box-Muller angle table fill;
+//     block-level sync follows the fill of the shared tables (Box-Muller
+//     angles, tire forces) at kernel entry;
 //   * particles never touch memory: noise (one Philox4x32-7 block per
 //     particle-step, philox.cuh), re-projection x = mu + L z, the
 //     Euler step, process noise and the moment sums all stay in registers;

@@ -37,10 +37,8 @@ struct VehDev {
   float drive, vfloor, rrf, rrr, spin_scale, dt;
   // front/rear lane pairs of the packed (FFMA2) particle step
   float2 lf_nlr;   // (lf, -lr)
-  float2 By_s;     // (Byf, -Byr): B alpha with alpha_r = -atan2(.) folded in
-  float2 Cy, Dy;   // (Cyf, Cyr), (Dyf, Dyr)
+  float2 Dy;       // (Dyf, Dyr)
   float2 Bx, Cx;   // (Bxf, Bxr), (Cxf, Cxr): longitudinal pair of step_shared
-  float2 nBy;      // (-Byf, -Byr): the lateral-slip pair as one FFMA2 on (atan2 f, atan2 r)
   float dt_lf_iz, ndt_lr_iz;   // dt lf / Iz, -dt lr / Iz: the yaw-rate Euler update
   float dt_m;                  // dt / m: the (vx, vy) Euler update
   // lateral magic formula sin(C atan(B alpha)) = alpha q(|alpha|) as a
@@ -243,7 +241,6 @@ struct StepShared {
   float2 nsd_cd;              // (-sin delta, cos delta)
   float2 rev;                 // atan2 quadrant fold: (1, 0) for vx_eff > 0, (-1, pi) below
   float2 dycx;                // (Dyf |cos|_f, Dyr |cos|_r): lateral peak x friction ellipse
-  float2 byd;                 // (Byf delta, 0): front slip-angle offset of the lateral pair
 };
 
 // kap: kappa(x[7]), supplied by the caller (the rollout already has it from
@@ -292,7 +289,6 @@ __device__ __forceinline__ StepShared step_shared(const float x[8], const CtlDev
   h.nsd_cd = make_float2(-c.sd, c.cd);
   h.rev = (h.vxe >= 0.f) ? make_float2(1.f, 0.f) : make_float2(-1.f, 3.14159265358979f);
   h.dycx = __fmul2_rn(V.Dy, h.cx);
-  h.byd = make_float2(V.Byf * c.delta, 0.f);
   // _derivs_row wheel torque balance; rolling resistance opposes the spin
 #ifdef BSS_EXACT_MATH
   const float spf = tanhf(wf * V.spin_scale), spr = tanhf(wr * V.spin_scale);
@@ -355,17 +351,18 @@ __device__ __forceinline__ bool step_particle(float x[8], const StepShared &h, c
 }
 
 #else
-// q(|alpha|) of one axle from its table rows: nearest-row index by the
-// 1.5 2^23 rounding trick (the row number ends up in the low mantissa bits,
-// no F2I), the in-cell offset by one FFMA, the cubic by three.  NaN / inf
-// arguments read row 0 and propagate through f.
+// Shared-window address of the block's tire-table copy, kept in a register.
 __device__ __forceinline__ uint32_t tire_tab_addr() {
   uint32_t v = (uint32_t)__cvta_generic_to_shared(g_tire_tab);
   asm volatile("" : "+r"(v));   // opaque: kept in a register (philox.cuh opaque_u32)
   return v;
 }
 
-// base: tire_tab_addr() of the calling block (TS only)
+// q(|alpha|) of one axle from its table rows: nearest-row index by the
+// 1.5 2^23 rounding trick (the row number ends up in the low mantissa bits,
+// no F2I), the in-cell offset by one FFMA, the cubic by three.  NaN / inf
+// arguments read row 0 and propagate through f.  TS: the block's shared
+// copy at base = tire_tab_addr(), else global memory.
 template <bool TS>
 __device__ __forceinline__ float tire_q(float a, const VehDev &V, int axle, uint32_t base) {
   const float MAGIC = 12582912.0f;   // 1.5 2^23
