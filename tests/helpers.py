@@ -153,3 +153,18 @@ def fp32_state_floor(inp, ks=None):
                     round_state=np.float32)
     mean, cov = np.stack([r[0] for r in rec]), np.stack([r[1] for r in rec])
     return (mean, cov) if ks is None else (mean[:, ks], cov[:, ks])
+
+
+def death_mismatches_weightless(gpu, ref, lam=1.0, span=100.0):
+    """Rollouts dead (+inf) in exactly one of two FP32 / FP64 runs of the same
+    batch: (count, all weightless).  A rollout that leaves the curvilinear
+    frame near the end of the horizon can die one step apart in FP32 and
+    FP64 (the frame check is a sharp threshold on a chaotic off-track
+    trajectory); such a rollout must carry no weight, i.e. its finite cost
+    sits more than span * lambda above the best one."""
+    import numpy as np
+    gf, rf = np.isfinite(gpu), np.isfinite(ref)
+    mism = gf != rf
+    best = min(np.min(gpu[gf]) if gf.any() else np.inf, np.min(ref[rf]) if rf.any() else np.inf)
+    alive_cost = np.where(rf, ref, gpu)
+    return int(mism.sum()), bool(np.all(alive_cost[mism] - best > span * lam))

@@ -6,6 +6,7 @@ K=65536 x M=64 x T=50, Laplace(0.03) + U(+-0.05) slip noise, shield beta=0.2,
 import numpy as np
 import pytest
 
+from helpers import death_mismatches_weightless
 from oracle import c_oracle
 from paper_2408_00494_b200 import controllers as mc
 from paper_2408_00494_b200 import dynamics as md
@@ -47,7 +48,9 @@ def test_c4_device_vs_extended_oracle():
                                   cfg.sigma_eps, cfg.precision, cfg.bounds, False, ctx)
     ref, _ = c_oracle.rollout(prob, x0, np.zeros((4, 4)), nominal, u=u, eps=eps, key_belief=kb)
     fin = np.isfinite(ref) & np.isfinite(gpu)
-    assert np.mean(np.isfinite(ref) == np.isfinite(gpu)) > 0.999
+    n_mism, weightless = death_mismatches_weightless(gpu, ref)
+    print(f"C4: dead in one of device / oracle only: {n_mism} of {cfg.samples}")
+    assert n_mism <= 1e-3 * cfg.samples and weightless
     rel = np.abs(gpu[fin] - ref[fin]) / np.abs(ref[fin])
     w = fin & (ref - ref[fin].min() <= 100.0)
     werr = np.max(np.abs(gpu[w] - ref[w]) / ref[w])

@@ -2,7 +2,8 @@
 noise arrays would be multi-GB: the device (Philox mode) against the FP64 C
 oracle driving the SAME Philox4x32 counters on the host (oracle/bss_oracle.c,
 pinned to the reference by tests/test_c_oracle.py).  The two differ only by
-FP32 vs FP64 arithmetic and MUFU vs libm Box-Muller (~1e-7 on the normals).
+FP32 vs FP64 arithmetic and the device Box-Muller (MUFU radius, tabulated
+angles) vs libm (~1e-7 on the normals).
 These shapes exercise the narrowed lane groups (G = 8) of large K and the
 512-thread one-wave launches (C2; a ragged 2047-rollout shard whose last
 block is partial)."""
@@ -10,7 +11,7 @@ block is partial)."""
 import numpy as np
 import pytest
 
-from helpers import channel_spread, moments_err_arrays, unpack_moments
+from helpers import channel_spread, death_mismatches_weightless, moments_err_arrays, unpack_moments
 
 from oracle import c_oracle
 from paper_2408_00494_b200 import _lib
@@ -44,7 +45,9 @@ def test_fullsize_philox_costs_and_update(K, M, T, dt):
     ref, _, rmom = c_oracle.rollout(prob, x0, np.zeros((4, 4)), nominal, u=u, eps=eps, key_belief=kb,
                                     moments=True)
     fin = np.isfinite(ref)
-    assert np.mean(np.isfinite(gpu) == fin) > 0.999
+    n_mism, weightless = death_mismatches_weightless(gpu, ref)
+    print(f"K={K} M={M}: dead in one of device / oracle only: {n_mism} of {K}")
+    assert n_mism <= 1e-3 * K and weightless
     both = fin & np.isfinite(gpu)
     rel = np.abs(gpu[both] - ref[both]) / np.abs(ref[both])
     weighted = both & (ref - ref[fin].min() <= 100.0)
