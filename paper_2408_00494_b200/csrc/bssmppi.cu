@@ -593,6 +593,22 @@ int finish(bssmppi_ctx *c, double *vplus, bssmppi_diag *diag) {
   return BSSMPPI_OK;
 }
 
+// The device's Box-Muller angle table (philox.cuh g_angle_global), built once
+// per device before its first rollout or statistics launch.
+int ensure_angle_table(int device) {
+  static std::mutex mu;
+  static std::vector<int> done;
+  std::lock_guard<std::mutex> lock(mu);
+  for (int d : done)
+    if (d == device) return BSSMPPI_OK;
+  angle_table_init_kernel<<<kAngleTab / 256, 256>>>();
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return fail(BSSMPPI_ERR_CUDA, "angle table: %s", cudaGetErrorString(e));
+  done.push_back(device);
+  return BSSMPPI_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -630,6 +646,7 @@ int bssmppi_create(const bssmppi_problem *problem, int32_t device, bssmppi_ctx *
   if (device < 0 || device >= ndev) return fail(BSSMPPI_ERR_INVALID, "device %d out of range", device);
   DeviceGuard guard(device);
   CUDA_TRY(cudaSetDevice(device));
+  if ((rc = ensure_angle_table(device))) return rc;
   bssmppi_ctx *c = new bssmppi_ctx();
   c->device = device;
   c->kind = problem->kind;
@@ -1096,8 +1113,12 @@ int bssmppi_tire_table(const double bc[4], double steer_max, float *out, int32_t
 
 int bssmppi_belief_normals(const uint32_t key[2], int32_t t, int32_t k, int32_t m_count, float *out) {
   if (!key || !out || m_count < 1) return fail(BSSMPPI_ERR_INVALID, "bad belief_normals arguments");
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int rc = ensure_angle_table(dev);
+  if (rc) return rc;
   float *d = nullptr;
-  int rc = dev_alloc(&d, (size_t)m_count * 7);
+  rc = dev_alloc(&d, (size_t)m_count * 7);
   if (rc) return rc;
   belief_normals_kernel<<<(m_count + 127) / 128, 128>>>(key[0], key[1], t, k, m_count, d);
   cudaError_t e = cudaGetLastError();

@@ -134,18 +134,25 @@ __device__ __forceinline__ float word_radius(uint32_t w) {
   const float u1 = kU1Mid - __uint_as_float(0x3f800000u + ((w & 0xfffff000u) >> 9));
   return sqrt_approx(-lg2_approx(u1));
 }
-// Angle grid (cos, sin)(2 pi j / 4096) = sincospi(j / 2048), j = w & 0xfff:
-// an exact-argument FP32 sincospif (<= 1 ulp), identical whether it is read
-// from a block's shared-memory table or evaluated in place.  The rollout
-// kernels tabulate the 4096 entries once per block (32 KB) and look the
-// pair up with one LDS.64: no MUFU.SIN / MUFU.COS and no angle arithmetic
-// per normal pair, and an error of 1 ulp instead of MUFU's 2^-21.4 absolute.
+// Angle grid (cos, sin)(2 pi j / 4096), j = w & 0xfff, correctly rounded to
+// FP32 from FP64 sincospi (one table per device, `angle_table_init_kernel`,
+// built once before the first rollout).  The rollout kernels copy it into a
+// per-block shared table (32 KB) and look a pair up with one LDS.64: no
+// MUFU.SIN / MUFU.COS and no angle arithmetic per normal pair, and half an
+// ulp of error instead of MUFU's 2^-21.4 absolute.  Persist blocks and the
+// statistics hook read the device table itself (the same values).
 constexpr int kAngleTab = 4096;
-__device__ __forceinline__ float2 angle_entry(uint32_t j) {
-  float s, c;
-  sincospif((float)j * (1.0f / 2048.0f), &s, &c);
-  return make_float2(c, s);
+__device__ float2 g_angle_global[kAngleTab];
+
+__global__ void angle_table_init_kernel() {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= kAngleTab) return;
+  double s, c;
+  sincospi((double)j / 2048.0, &s, &c);
+  g_angle_global[j] = make_float2((float)c, (float)s);
 }
+
+__device__ __forceinline__ float2 angle_entry(uint32_t j) { return __ldg(&g_angle_global[j]); }
 
 // The table of a rollout block (filled by bss_rollout_kernel; kernels that
 // never name it do not allocate it).

@@ -759,13 +759,27 @@ __device__ __forceinline__ void bss_rollout_nk(const RollParams &P) {
 // shapes of bssmppi.cu rollout_block_threads); same register budget.
 template <int G, bool PERSIST, bool ZARR, int BT = kBlockThreads>
 __global__ void BSS_ROLLOUT_BOUNDS bss_rollout_kernel(const RollParams P) {
-  // Shared tables, built once per block -- the Box-Muller angle table
-  // (philox.cuh angle_entry) and a copy of the tire table (vehicle.cuh;
-  // persist blocks keep their shared memory for the clouds) -- then the
-  // kernel's one block-wide barrier, before any warp can retire.
+  // Shared tables, copied once per block -- the Box-Muller angle table
+  // (philox.cuh g_angle_global, two entries per 16-byte load) and the tire
+  // table (vehicle.cuh; persist blocks keep their shared memory for the
+  // clouds) -- then the kernel's one block-wide barrier, before any warp
+  // can retire.
   const bool ts = !PERSIST && P.V.tire_smem;
-  if (!PERSIST && !ZARR)
-    for (int j = threadIdx.x; j < kAngleTab; j += BT) g_angle_tab[j] = angle_entry((uint32_t)j);
+  if (!PERSIST && !ZARR) {
+    const float4 *src = reinterpret_cast<const float4 *>(g_angle_global);
+    float4 *dst = reinterpret_cast<float4 *>(g_angle_tab);
+    static_assert((kAngleTab / 2) % BT == 0, "angle table copy: whole rounds per thread");
+    constexpr int R = kAngleTab / 2 / BT;
+    constexpr int CH = R < 8 ? R : 8;       // up to 8 loads in flight before their stores
+#pragma unroll
+    for (int i0 = 0; i0 < R; i0 += CH) {
+      float4 v[CH];
+#pragma unroll
+      for (int i = 0; i < CH; ++i) v[i] = __ldg(src + threadIdx.x + (i0 + i) * BT);
+#pragma unroll
+      for (int i = 0; i < CH; ++i) dst[threadIdx.x + (i0 + i) * BT] = v[i];
+    }
+  }
   if (ts)
     for (int j = threadIdx.x; j < 2 * P.V.tire_rows; j += BT) {
       const int axle = j >= P.V.tire_rows, row = j - axle * P.V.tire_rows;
