@@ -601,9 +601,16 @@ int ensure_angle_table(int device) {
   std::lock_guard<std::mutex> lock(mu);
   for (int d : done)
     if (d == device) return BSSMPPI_OK;
-  angle_table_init_kernel<<<kAngleTab / 256, 256>>>();
-  cudaError_t e = cudaGetLastError();
-  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  // on a private non-blocking stream: no implicit synchronisation with
+  // work the caller already has in flight on the device
+  cudaStream_t st = nullptr;
+  cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (e == cudaSuccess) {
+    angle_table_init_kernel<<<kAngleTab / 256, 256, 0, st>>>();
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+  }
   if (e != cudaSuccess) return fail(BSSMPPI_ERR_CUDA, "angle table: %s", cudaGetErrorString(e));
   done.push_back(device);
   return BSSMPPI_OK;
