@@ -123,9 +123,8 @@ CASES = [
                       b_long_front=2.5, c_long_front=1.6, b_long_rear=1.8, c_long_rear=1.5,
                       peak_fx_front=90.0, peak_fy_front=100.0, peak_fx_rear=110.0, peak_fy_rear=95.0,
                       drive_gain=10.0, roll_resist=0.02, v_floor=0.4)),
-    # wide lateral shape factors (C pi / 2 > 2.2): the kernels' full-range
-    # tire sine (fastmath.cuh sin_tire_x2<false>); the cases above all take
-    # the short form
+    # wide lateral shape factors (C = 1.9 / 1.7): a different per-vehicle
+    # tire table (csrc/bssmppi.cu tire_table_host) than the default tire
     dict(name="wide_tire", track="ellipse", K=64, M=24, T=15, dt=0.05, seed=38, run_path=[7],
          warm=1, sigma_eps=[[0.2 ** 2, 0], [0, 0.5 ** 2]], noise=[0.03, 0.03, 0.06],
          x0=dict(vx=5.0, s=14.0, e_y=0.3), kind="bss", persist=False,

@@ -139,7 +139,8 @@ def main():
         return
     if what == "sin_tire":
         # sin x = x (1 + t Q(t)) on |x| <= 2.2 with Q of degree 4 (constant term of
-        # the bracket held at 1): the short lateral tire sine (fastmath.cuh sin_tire_x2)
+        # the bracket held at 1): the short lateral tire sine of round 1 (now
+        # replaced by the per-vehicle tire table, vehicle.cuh tire_q)
         xs = np.linspace(1e-5, 2.2, 40001)
         t = xs * xs
         g = (np.sin(xs) / xs - 1.0) / t
