@@ -337,7 +337,8 @@ void fill_params(bssmppi_ctx *c, const bssmppi_problem *p) {
 // the narrower grid keeps the SMs busy:
 //   (1) to >= 8 particles per lane while >= 1024 warps remain;
 //   (2) to <= 64 particles per lane while >= 4096 warps remain (~1.7 waves
-//       of 16 warps x 148 SMs).
+//       of 16 warps x 148 SMs), down to G = 2 (M = 64 at K >= 65536: 3.88 vs
+//       4.16 ms at 131072 x 64 x 60, 1.68 vs 1.79 ms at 65536 x 64 x 50).
 // Fitted to a G sweep over 14 (K, M) shapes with the pipelined kernel
 // (tools/g_sweep.sh, profiles/r1_group_width_sweep.txt): it picks the best
 // or a tied G on every one.  Decided on the LOCAL rollout count, so a
@@ -351,7 +352,7 @@ int group_width(int M, int K) {
   while (g < M && g < 32) g <<= 1;
   const auto warps = [K](int gg) { return (long long)K * gg / 32; };
   while (g > 4 && M < 8 * g && warps(g / 2) >= 1024) g >>= 1;
-  while (g > 4 && M < 64 * g && warps(g / 2) >= 4096) g >>= 1;
+  while (g > 2 && M < 64 * g && warps(g / 2) >= 4096) g >>= 1;
   return g;
 }
 

@@ -4,9 +4,9 @@ oracle driving the SAME Philox4x32 counters on the host (oracle/bss_oracle.c,
 pinned to the reference by tests/test_c_oracle.py).  The two differ only by
 FP32 vs FP64 arithmetic and the device Box-Muller (MUFU radius, tabulated
 angles) vs libm (~1e-7 on the normals).
-These shapes exercise the narrowed lane groups (G = 8) of large K and the
-512-thread one-wave launches (C2; a ragged 2047-rollout shard whose last
-block is partial)."""
+These shapes exercise the narrowed lane groups of large K (G = 8 at C3, 4 at
+C5 32768 x 64, 2 at the C4 shape 65536 x 64) and the 512-thread one-wave
+launches (C2; a ragged 2047-rollout shard whose last block is partial)."""
 
 import numpy as np
 import pytest
@@ -23,8 +23,8 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("K,M,T,dt", [(16384, 256, 50, 0.04), (32768, 64, 60, 0.04), (4096, 128, 40, 0.05),
-                                     (2047, 256, 20, 0.05)],
-                         ids=["C3", "C5_32768x64", "C2", "ragged_one_wave"])
+                                     (2047, 256, 20, 0.05), (65536, 64, 50, 0.04)],
+                         ids=["C3", "C5_32768x64", "C2", "ragged_one_wave", "C4_shape_G2"])
 def test_fullsize_philox_costs_and_update(K, M, T, dt):
     track = named_track("spline0" if dt == 0.04 else "ellipse")
     model = md.with_timestep(md.VehicleParams(), dt, "euler")

@@ -248,4 +248,5 @@ def test_group_width_policy():
     assert gw(64, 4096) == 8            # C5 4096 x 64: 8 particles per lane
     assert gw(128, 4096) == 16          # C2
     assert gw(512, 4096) == 32 and gw(512, 32768) == 8
-    assert gw(64, 65536) == 4           # C4
+    assert gw(64, 65536) == 2           # C4, C5 65536+ x 64: 32 particles per lane
+    assert gw(64, 131072) == 2 and gw(256, 131072) == 4 and gw(512, 131072) == 8
