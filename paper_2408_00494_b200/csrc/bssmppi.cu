@@ -336,6 +336,11 @@ void fill_params(bssmppi_ctx *c, const bssmppi_problem *p) {
 // so narrower groups amortise it over more particles per lane -- as long as
 // the narrower grid keeps the SMs busy:
 //   (1) to >= 8 particles per lane while >= 1024 warps remain;
+//   (1b) to >= 16 particles per lane while >= 1400 warps remain (measured
+//       between 1024 warps, where the wider group wins by 4-6% -- 2048 x 256,
+//       4096 x 128, 8192 x 64 -- and 1500, where the narrower one wins by
+//       9-10% -- 3000 x 256, 12000 x 64; also 4096 x 256 -5.5%,
+//       8192 x 128 -5.6%, 16384 x 64 -7%; profiles/README.md);
 //   (2) to <= 64 particles per lane while >= 4096 warps remain (~1.7 waves
 //       of 16 warps x 148 SMs), down to G = 2 (M = 64 at K >= 65536: 3.88 vs
 //       4.16 ms at 131072 x 64 x 60, 1.68 vs 1.79 ms at 65536 x 64 x 50).
@@ -352,6 +357,7 @@ int group_width(int M, int K) {
   while (g < M && g < 32) g <<= 1;
   const auto warps = [K](int gg) { return (long long)K * gg / 32; };
   while (g > 4 && M < 8 * g && warps(g / 2) >= 1024) g >>= 1;
+  while (g > 4 && M < 16 * g && warps(g / 2) >= 1400) g >>= 1;
   while (g > 2 && M < 64 * g && warps(g / 2) >= 4096) g >>= 1;
   return g;
 }

@@ -234,8 +234,8 @@ def test_default_subset():
 
 def test_group_width_policy():
     """Lanes per rollout (csrc/bssmppi.cu group_width): one warp for small
-    problems; >= 8 particles per lane while >= 1024 warps remain, then up to
-    64 per lane while >= 4096 warps remain -- the measured best G on every
+    problems; >= 8 particles per lane while >= 1024 warps remain, >= 16 while
+    >= 1400 remain, then up to 64 per lane while >= 4096 warps remain -- the measured best G on every
     swept shape (profiles/r1_group_width_sweep.txt)."""
     from paper_2408_00494_b200 import _lib
     gw = _lib.load().bssmppi_group_width
@@ -243,6 +243,9 @@ def test_group_width_policy():
     assert gw(256, 16384) == 8          # C3 on one GPU
     assert gw(256, 8192) == 16          # C3 shard at 2 GPUs
     assert gw(256, 2048) == 32          # C3 shard at 8 GPUs
+    assert gw(256, 4096) == 16          # C3 shard at 4 GPUs: 16 particles per lane, 2048 warps
+    assert gw(256, 3000) == 16 and gw(128, 8192) == 8 and gw(64, 16384) == 4 and gw(64, 12000) == 4
+    assert gw(64, 8192) == 8            # C4 shard at 8 GPUs: 1024 warps at G = 4 are too few
     assert gw(256, 32768) == 4          # 64 particles per lane
     assert gw(64, 32768) == 4           # C5 32768 x 64
     assert gw(64, 4096) == 8            # C5 4096 x 64: 8 particles per lane
