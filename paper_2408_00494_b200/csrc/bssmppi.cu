@@ -369,9 +369,17 @@ size_t persist_smem(int g, int M) {
          (size_t)(kBlockThreads / g) * 8 * M * sizeof(float);
 }
 
-// forced: bssmppi_problem.group_width (0 = the policy above).
+// forced: bssmppi_problem.group_width (0 = the policy above).  Persist mode
+// is not narrowed: its clouds live in shared memory ([8][M] floats per
+// rollout), so a narrow group means few resident blocks -- at C3 G = 8 holds
+// one 128 KB block per SM and runs 9.54 ms against 4.22 ms at G = 32
+// (tools/persist_sweep.py: G = 32 or a tie on every shape).
 int rollout_group_width(int M, int K, bool persist, int forced = 0) {
   int g = forced ? forced : group_width(M, K);
+  if (persist && !forced) {
+    g = 2;
+    while (g < M && g < 32) g <<= 1;
+  }
   while (persist && g < 32 && persist_smem(g, M) > kSmemMax) g <<= 1;
   return g;
 }

@@ -44,7 +44,7 @@ def _run(K, M, T, persist=False, dt=0.05, seed=0):
     (33, 7, 3, False),           # ragged K (33 groups of 8) and M (7 of 8 lanes busy)
     (2, 8192, 3, False),         # ABI maximum inner_samples (256 particles per lane)
     (16, 4, 512, False),         # ABI maximum horizon
-    (16384, 512, 3, True),       # persist at large K: policy G = 8 widened to fit the clouds
+    (16384, 512, 3, True),       # persist at large K: the group is not narrowed (G = 32, 64 KB of clouds per block)
     (2, 1792, 2, True),          # the largest persist cloud (G = 32 block)
 ], ids=["K1M2T1", "M3", "ragged", "Mmax", "Tmax", "persist_wide", "persist_max"])
 def test_edge_shape_costs_match_oracle(K, M, T, persist):
